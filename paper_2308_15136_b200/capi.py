@@ -1,0 +1,161 @@
+"""ctypes bindings for the C-ABI boundary, include/cagra/capi.h.
+
+This is exactly the binding a Python user of the reference would add
+(INTEGRATION.md shows the cgo and ctypes stubs).  The shared library is built
+in-tree by `make` / `__graft_entry__.build()`; importing this module without it
+fails loudly — there is no CPU fallback behind this API.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcagra_b200.so")
+
+OK, ERR_USAGE, ERR_FORMAT, ERR_CUDA, ERR_NCCL, ERR_LOGIC = 0, 2, 3, 4, 5, 6
+HASH_STANDARD, HASH_FORGETTABLE = 0, 1
+MODE_PER_QUERY, MODE_SHARED = 0, 1
+INVALID_ID = 0xFFFFFFFF
+
+
+class CagraError(RuntimeError):
+    code = -1
+
+
+class UsageError(CagraError, ValueError):
+    """fodg::UsageError (common.hpp:13-15)."""
+    code = ERR_USAGE
+
+
+class FormatError(CagraError):
+    """fodg::FormatError (common.hpp:18-20)."""
+    code = ERR_FORMAT
+
+
+class CudaError(CagraError):
+    code = ERR_CUDA
+
+
+class LogicError(CagraError):
+    """std::logic_error (search.cpp:180)."""
+    code = ERR_LOGIC
+
+
+_ERRORS = {ERR_USAGE: UsageError, ERR_FORMAT: FormatError, ERR_CUDA: CudaError,
+           ERR_LOGIC: LogicError, ERR_NCCL: CagraError}
+
+
+class SearchParamsC(C.Structure):
+    _fields_ = [("k", C.c_uint32), ("topm", C.c_uint32), ("width", C.c_uint32),
+                ("max_iterations", C.c_uint32), ("min_iterations", C.c_uint32),
+                ("hash_policy", C.c_uint32), ("hash_bits", C.c_uint32),
+                ("reset_interval", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class EngineOptsC(C.Structure):
+    _fields_ = [("mode", C.c_uint32), ("team_count", C.c_uint32), ("num_threads", C.c_uint32),
+                ("seed_mode", C.c_uint32), ("query_offset", C.c_uint64),
+                ("exact_distances", C.c_uint32), ("team_size", C.c_uint32)]
+
+
+class SearchStatsC(C.Structure):
+    _fields_ = [("iterations", C.c_uint32), ("hash_resets", C.c_uint32),
+                ("distance_evals", C.c_uint64), ("converged", C.c_uint32), ("_pad", C.c_uint32)]
+
+
+STATS_DTYPE = np.dtype([("iterations", np.uint32), ("hash_resets", np.uint32),
+                        ("distance_evals", np.uint64), ("converged", np.uint32),
+                        ("_pad", np.uint32)])
+
+
+class OptStatsC(C.Structure):
+    _fields_ = [("count_seconds", C.c_double), ("reorder_seconds", C.c_double),
+                ("reverse_seconds", C.c_double), ("merge_seconds", C.c_double),
+                ("total_seconds", C.c_double)]
+
+
+# Every symbol include/cagra/capi.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = [
+    "cagra_last_error", "cagra_version", "cagra_device_count", "cagra_search_params_default",
+    "cagra_engine_opts_default", "cagra_uniform_dataset", "cagra_mix_seed",
+    "cagra_exact_knn_graph", "cagra_exact_topk", "cagra_count_detourable_routes",
+    "cagra_reorder_and_prune", "cagra_build_reverse_graph", "cagra_merge_graphs",
+    "cagra_optimize", "cagra_build_graph", "cagra_index_create", "cagra_index_create_dev",
+    "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
+    "cagra_search_dev", "cagra_last_launch_count", "cagra_merge_shard_topk_dev",
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libcagra_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} missing: build the CUDA engine first (make, or "
+                "__graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        L.cagra_last_error.restype = C.c_char_p
+        L.cagra_version.restype = C.c_char_p
+        L.cagra_mix_seed.restype = u64
+        L.cagra_mix_seed.argtypes = [u64]
+        L.cagra_uniform_dataset.argtypes = [u64, u64, vp]
+        L.cagra_exact_knn_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
+        L.cagra_exact_topk.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp]
+        L.cagra_count_detourable_routes.argtypes = [vp, vp, u32, u32, i32, vp]
+        L.cagra_reorder_and_prune.argtypes = [vp, vp, u32, u32, u32, i32, vp]
+        L.cagra_build_reverse_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
+        L.cagra_merge_graphs.argtypes = [vp, vp, vp, u32, u32, u32, i32, vp]
+        L.cagra_optimize.argtypes = [vp, vp, u32, u32, u32, u32, u32, i32, vp, vp]
+        L.cagra_build_graph.argtypes = [vp, u32, u32, u32, u32, i32, vp, vp, vp, vp]
+        L.cagra_index_create.argtypes = [vp, u32, u32, vp, u32, i32, C.POINTER(vp)]
+        L.cagra_index_create_dev.argtypes = [vp, u32, u32, vp, u32, i32, C.POINTER(vp)]
+        L.cagra_index_destroy.argtypes = [vp]
+        L.cagra_index_info.argtypes = [vp, vp, vp, vp, vp]
+        L.cagra_index_row_stride.restype = u32
+        L.cagra_index_row_stride.argtypes = [vp]
+        L.cagra_search.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp, vp, vp]
+        L.cagra_search_dev.argtypes = [vp, vp, u32, vp, vp, vp, vp, vp, vp, vp]
+        L.cagra_last_launch_count.restype = u32
+        L.cagra_last_launch_count.argtypes = [vp]
+        L.cagra_merge_shard_topk_dev.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, i32, vp]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().cagra_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, CagraError)(msg)
+
+
+def ptr(a) -> C.c_void_p:
+    if a is None:
+        return C.c_void_p(0)
+    if isinstance(a, np.ndarray):
+        return C.c_void_p(a.ctypes.data)
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    return C.c_void_p(a.data_ptr())  # torch tensor (device pointers for *_dev)
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    lib().cagra_device_count(C.byref(c))
+    return c.value
+
+
+def mix_seed(x: int) -> int:
+    return int(lib().cagra_mix_seed(C.c_uint64(x & 0xFFFFFFFFFFFFFFFF)))
+
+
+def uniform_dataset(n: int, dim: int, seed: int) -> np.ndarray:
+    out = np.empty((n, dim), np.float32)
+    check(lib().cagra_uniform_dataset(C.c_uint64(seed), C.c_uint64(n * dim), ptr(out)))
+    return out

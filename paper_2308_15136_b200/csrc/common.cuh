@@ -1,0 +1,116 @@
+// Shared definitions for the B200-native CAGRA engine (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace cagra {
+
+// Node id layout, /root/reference/proj/core/include/fodg/common.hpp:22-27.
+constexpr uint32_t kIdMask = 0x7fffffffu;
+constexpr uint32_t kParentFlag = 0x80000000u;
+constexpr uint32_t kInvalidId = 0xffffffffu;
+constexpr uint64_t kMaxNodes = kIdMask;
+
+// A buffer entry packed into one 64-bit word: (dist bits << 32) | id-with-flag.
+// dist >= +0 always (sum of squares from +0), so the IEEE bit pattern orders
+// like the float; comparing with the flag bit masked reproduces entry_less
+// (search.hpp:35-38): (dist, stripped id).  The dummy {0xffffffff, +inf}
+// (search.hpp:44) is the maximum key.
+constexpr uint64_t kFlagBit64 = 0x80000000ull;
+constexpr uint64_t kDummyKey = 0x7f800000ffffffffull;
+
+__host__ __device__ __forceinline__ uint32_t f2u(float f) {
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(f);
+#else
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+#endif
+}
+__host__ __device__ __forceinline__ float u2f(uint32_t u) {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t cmp_key(uint64_t e) { return e & ~kFlagBit64; }
+__host__ __device__ __forceinline__ uint64_t make_key(float dist, uint32_t id) {
+  return (static_cast<uint64_t>(f2u(dist)) << 32) | id;
+}
+__host__ __device__ __forceinline__ uint32_t key_id(uint64_t e) {
+  return static_cast<uint32_t>(e);
+}
+__host__ __device__ __forceinline__ float key_dist(uint64_t e) {
+  return u2f(static_cast<uint32_t>(e >> 32));
+}
+__host__ __device__ __forceinline__ bool key_is_dummy(uint64_t e) {
+  return static_cast<uint32_t>(e) == kInvalidId;
+}
+
+// splitmix64 finaliser, common.hpp:34-39.
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// Knuth multiplicative hash, search.cpp:21-23.
+__host__ __device__ __forceinline__ uint32_t hash_id(uint32_t id, uint32_t mask) {
+  return (id * 2654435761u) & mask;
+}
+
+__host__ __device__ __forceinline__ uint32_t next_pow2_u32(uint32_t x) {
+  uint32_t c = 1;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+__host__ __device__ __forceinline__ uint32_t round_up_u32(uint32_t x, uint32_t m) {
+  return (x + m - 1) / m * m;
+}
+
+#ifdef __CUDACC__
+// The reference distance, dataset.hpp:33-43: strictly sequential fp32 chain,
+// separately rounded subtract, multiply and add (no FMA contraction).
+__device__ __forceinline__ float seq_step(float acc, float a, float b) {
+  float diff = __fsub_rn(a, b);
+  return __fadd_rn(acc, __fmul_rn(diff, diff));
+}
+#endif
+
+// ---- host-side error types; capi.cu maps them to status codes ----
+struct UsageErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct FormatErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct LogicErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+}  // namespace cagra
+
+#define CAGRA_CUDA_TRY(expr)                                                         \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      throw ::cagra::CudaErr(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+    }                                                                                \
+  } while (0)
+
+#define CAGRA_LAUNCH_CHECK() CAGRA_CUDA_TRY(cudaGetLastError())

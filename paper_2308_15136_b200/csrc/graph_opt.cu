@@ -1,0 +1,468 @@
+// Rank-mode graph optimization on device (graph_opt.cpp:45-246), bit-exact:
+//   K2 detour_reorder : count_detourable_routes (:45-96) fused with
+//                       reorder_and_prune (:98-124) — one CTA per node
+//   K3 reverse        : build_reverse_graph (:141-160) — count, scan, scatter,
+//                       per-row (rank, source) selection
+//   K4 merge          : merge_graphs (:162-209) — one warp per node
+// Integer work only; every output position is a pure function of the input
+// rows (atomics only accumulate counts or claim bucket slots that are sorted
+// afterwards), so results never depend on scheduling.
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cagra {
+namespace {
+
+constexpr int OPT_NT = 128;
+
+// ---------------------------------------------------------------- checks --
+__global__ void check_sorted_kernel(const uint32_t* __restrict__ ids,
+                                    const float* __restrict__ dists, uint32_t n, uint32_t deg,
+                                    int* flag) {
+  // graph_opt.cpp:19-31: (dist, id) strictly increasing along each row.
+  uint64_t total = (uint64_t)n * deg;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (e % deg == 0) continue;
+    float a = dists[e - 1], b = dists[e];
+    bool ok = a < b || (a == b && ids[e - 1] < ids[e]);
+    if (!ok) atomicOr(flag, 1);
+  }
+}
+
+__global__ void check_ids_kernel(const uint32_t* __restrict__ ids, uint64_t count, uint32_t n,
+                                 int* flag) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    if (ids[e] >= n) atomicOr(flag, 2);
+}
+
+// ------------------------------------------------------ block bitonic sort --
+__device__ void block_bitonic_sort(uint64_t* a, uint32_t P) {
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          uint64_t x = a[i], y = a[ixj];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K2 ---
+// Shared layout: xrow[deg] | hkey[H] | hrank[H] | counts[deg] | keys[P] (u64)
+__global__ void __launch_bounds__(OPT_NT)
+detour_reorder_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t deg, uint32_t d,
+                      uint32_t H, uint32_t P, const uint32_t* __restrict__ counts_in,
+                      uint32_t* __restrict__ counts_out, uint32_t* __restrict__ pruned_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* xrow = reinterpret_cast<uint32_t*>(keys + P);
+  uint32_t* hkey = xrow + deg;
+  uint32_t* hrank = hkey + H;
+  uint32_t* counts = hrank + H;
+  const uint32_t hmask = H - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+
+  for (uint32_t x = blockIdx.x; x < n; x += gridDim.x) {
+    const uint32_t* xr = knn + (size_t)x * deg;
+    for (uint32_t i = tid; i < H; i += blockDim.x) {
+      hkey[i] = kInvalidId;
+      hrank[i] = kInvalidId;
+    }
+    for (uint32_t r = tid; r < deg; r += blockDim.x) {
+      xrow[r] = xr[r];
+      counts[r] = 0;
+    }
+    __syncthreads();
+    if (counts_in == nullptr) {
+      // rank_of: first occurrence wins (unordered_map::emplace, graph_opt.cpp:62)
+      for (uint32_t r = tid; r < deg; r += blockDim.x) {
+        uint32_t id = xrow[r];
+        uint32_t h = hash_id(id, hmask);
+        for (;;) {
+          uint32_t old = atomicCAS(&hkey[h], kInvalidId, id);
+          if (old == kInvalidId || old == id) break;
+          h = (h + 1) & hmask;
+        }
+        atomicMin(&hrank[h], r);
+      }
+      __syncthreads();
+      // X -> Z (rank rz) -> Y (rank rzy in Z's row); X -> Y at rank ry.
+      // Only routes with max(rz, rzy) < ry count (graph_opt.cpp:74-93), so
+      // rz and rzy never need to reach deg-1.
+      for (uint32_t rz = warp; rz + 1 < deg; rz += nwarps) {
+        const uint32_t* zr = knn + (size_t)xrow[rz] * deg;
+        for (uint32_t rzy = lane; rzy + 1 < deg; rzy += 32) {
+          uint32_t y = __ldg(&zr[rzy]);
+          if (y == x) continue;
+          uint32_t h = hash_id(y, hmask);
+          uint32_t ry = kInvalidId;
+          for (;;) {
+            uint32_t k = hkey[h];
+            if (k == y) {
+              ry = hrank[h];
+              break;
+            }
+            if (k == kInvalidId) break;
+            h = (h + 1) & hmask;
+          }
+          if (ry == kInvalidId || ry == rz) continue;
+          uint32_t mx = rz > rzy ? rz : rzy;
+          if (mx < ry) atomicAdd(&counts[ry], 1u);
+        }
+      }
+      __syncthreads();
+    } else {
+      for (uint32_t r = tid; r < deg; r += blockDim.x) counts[r] = counts_in[(size_t)x * deg + r];
+      __syncthreads();
+    }
+    if (counts_out)
+      for (uint32_t r = tid; r < deg; r += blockDim.x) counts_out[(size_t)x * deg + r] = counts[r];
+    if (pruned_out) {
+      // stable sort by count == sort by (count, initial rank)
+      for (uint32_t i = tid; i < P; i += blockDim.x)
+        keys[i] = i < deg ? ((uint64_t)counts[i] << 32) | i : ~0ull;
+      __syncthreads();
+      block_bitonic_sort(keys, P);
+      for (uint32_t j = tid; j < d; j += blockDim.x)
+        pruned_out[(size_t)x * d + j] = xrow[(uint32_t)keys[j]];
+    }
+    __syncthreads();
+  }
+}
+
+size_t detour_smem(uint32_t deg, uint32_t H, uint32_t P) {
+  return sizeof(uint64_t) * P + sizeof(uint32_t) * (deg + 2 * H + deg);
+}
+
+// ------------------------------------------------------------------- K3 ---
+__global__ void indeg_kernel(const uint32_t* __restrict__ pruned, uint64_t edges,
+                             uint32_t* __restrict__ indeg) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < edges;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&indeg[pruned[e]], 1u);
+}
+
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_PER = 4;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_PER;
+
+// block-local exclusive scan of SCAN_TILE values; returns block total
+__device__ unsigned long long block_scan_tile(const uint32_t* in, uint32_t n, uint32_t base,
+                                              unsigned long long* out, unsigned long long carry) {
+  __shared__ unsigned long long warp_tot[SCAN_NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long v[SCAN_PER];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; ++i) {
+    uint32_t idx = base + tid * SCAN_PER + i;
+    v[i] = idx < n ? in[idx] : 0;
+    local += v[i];
+  }
+  unsigned long long incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  unsigned long long woff = 0, total = 0;
+  for (int w = 0; w < SCAN_NT / 32; ++w) {
+    if (w < warp) woff += warp_tot[w];
+    total += warp_tot[w];
+  }
+  unsigned long long run = carry + woff + incl - local;
+#pragma unroll
+  for (int i = 0; i < SCAN_PER; ++i) {
+    uint32_t idx = base + tid * SCAN_PER + i;
+    if (out && idx < n) out[idx] = run;
+    run += v[i];
+  }
+  __syncthreads();
+  return total;
+}
+
+__global__ void scan_partial_kernel(const uint32_t* in, uint32_t n,
+                                    unsigned long long* block_sums) {
+  unsigned long long t = block_scan_tile(in, n, blockIdx.x * SCAN_TILE, nullptr, 0);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = t;
+}
+
+__global__ void scan_block_sums_kernel(unsigned long long* sums, uint32_t nb) {
+  // single CTA, sequential over tiles of block sums (exclusive, in place)
+  __shared__ unsigned long long tile[SCAN_TILE];
+  __shared__ unsigned long long carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < nb; b0 += SCAN_TILE) {
+    for (int i = threadIdx.x; i < SCAN_TILE; i += SCAN_NT)
+      tile[i] = b0 + i < nb ? sums[b0 + i] : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long c = carry_s;
+      for (int i = 0; i < SCAN_TILE && b0 + i < nb; ++i) {
+        unsigned long long t = tile[i];
+        sums[b0 + i] = c;
+        c += t;
+      }
+      carry_s = c;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void scan_final_kernel(const uint32_t* in, uint32_t n,
+                                  const unsigned long long* block_sums,
+                                  unsigned long long* out) {
+  block_scan_tile(in, n, blockIdx.x * SCAN_TILE, out, block_sums[blockIdx.x]);
+}
+
+__global__ void set_total_kernel(const uint32_t* in, uint32_t n, unsigned long long* out) {
+  out[n] = out[n - 1] + in[n - 1];
+}
+
+__global__ void reverse_scatter_kernel(const uint32_t* __restrict__ pruned, uint32_t n,
+                                       uint32_t d, const unsigned long long* __restrict__ start,
+                                       uint32_t* __restrict__ fill, uint64_t* __restrict__ keys) {
+  uint64_t edges = (uint64_t)n * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < edges;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)(e / d), r = (uint32_t)(e % d);
+    uint32_t y = pruned[e];
+    uint32_t pos = atomicAdd(&fill[y], 1u);
+    keys[start[y] + pos] = ((uint64_t)r << 32) | x;  // order (rank, source)
+  }
+}
+
+constexpr int REV_WARPS = 8;
+constexpr int REV_BUF = 1024;  // per-warp key buffer
+
+// Warp per target node y: the `cap` smallest (rank, source) keys of its
+// bucket, processed in chunks so any in-degree works.
+__global__ void __launch_bounds__(REV_WARPS * 32)
+reverse_select_kernel(const unsigned long long* __restrict__ start,
+                      const uint64_t* __restrict__ keys, uint32_t n, uint32_t cap,
+                      uint32_t* __restrict__ rev_counts, uint32_t* __restrict__ rev_ids) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + warp * REV_BUF;
+  const uint32_t capP = next_pow2_u32(cap);
+  const uint32_t chunk = REV_BUF - capP;
+  for (uint32_t y = blockIdx.x * REV_WARPS + warp; y < n; y += gridDim.x * REV_WARPS) {
+    unsigned long long b = start[y], e = start[y + 1];
+    uint32_t len = (uint32_t)(e - b);
+    uint32_t have = 0;  // sorted best prefix in buf[0..have)
+    for (uint32_t off = 0; off < len; off += chunk) {
+      uint32_t take = min(chunk, len - off);
+      uint32_t tot = have + take;
+      uint32_t P = next_pow2_u32(tot);
+      for (uint32_t i = lane; i < P; i += 32) {
+        if (i >= have) buf[i] = (i < tot) ? keys[b + off + (i - have)] : ~0ull;
+      }
+      __syncwarp();
+      for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = lane; i < P; i += 32) {
+            uint32_t ixj = i ^ j;
+            if (ixj > i) {
+              uint64_t u = buf[i], v = buf[ixj];
+              bool up = (i & k) == 0;
+              if ((u > v) == up) {
+                buf[i] = v;
+                buf[ixj] = u;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      have = min(tot, cap);
+    }
+    for (uint32_t i = lane; i < have; i += 32) rev_ids[(size_t)y * cap + i] = (uint32_t)buf[i];
+    if (lane == 0) rev_counts[y] = have;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------- K4 ---
+constexpr int MRG_WARPS = 4;
+
+// Warp per node: the reference's sequential interleave (graph_opt.cpp:177-206),
+// with the "already emitted" test done by all 32 lanes against the emitted
+// prefix (ballot) instead of a serial scan.
+__global__ void __launch_bounds__(MRG_WARPS * 32)
+merge_kernel(const uint32_t* __restrict__ pruned, const uint32_t* __restrict__ rev_counts,
+             const uint32_t* __restrict__ rev_ids, uint32_t n, uint32_t d, uint32_t rev_cap,
+             uint32_t* __restrict__ out, int* flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* P = reinterpret_cast<uint32_t*>(smem_raw) + warp * (2 * d + rev_cap);
+  uint32_t* R = P + d;
+  uint32_t* E = R + rev_cap;
+  for (uint32_t v = blockIdx.x * MRG_WARPS + warp; v < n; v += gridDim.x * MRG_WARPS) {
+    uint32_t rlen = rev_counts[v];
+    for (uint32_t i = lane; i < d; i += 32) P[i] = pruned[(size_t)v * d + i];
+    for (uint32_t i = lane; i < rlen; i += 32) R[i] = rev_ids[(size_t)v * rev_cap + i];
+    __syncwarp();
+    uint32_t pi = 0, ri = 0, emitted = 0;
+    bool ok = true;
+    for (uint32_t slot = 0; slot < d && ok; ++slot) {
+      bool got = false;
+      uint32_t id = 0;
+      for (int attempt = 0; attempt < 2 && !got; ++attempt) {
+        bool from_p = ((slot & 1) == 0) != (attempt == 1);
+        const uint32_t* src = from_p ? P : R;
+        uint32_t len = from_p ? d : rlen;
+        uint32_t& pos = from_p ? pi : ri;
+        while (pos < len && !got) {
+          uint32_t cand = src[pos++];
+          bool dup = false;
+          for (uint32_t j0 = 0; j0 < emitted && !dup; j0 += 32) {
+            uint32_t j = j0 + lane;
+            dup = __any_sync(0xffffffffu, j < emitted && E[j] == cand);
+          }
+          if (!dup) {
+            id = cand;
+            got = true;
+          }
+        }
+      }
+      if (!got) {
+        ok = false;
+        break;
+      }
+      if (lane == 0) E[emitted] = id;
+      __syncwarp();
+      ++emitted;
+    }
+    if (!ok) {
+      if (lane == 0) atomicOr(flag, 4);
+    } else {
+      for (uint32_t i = lane; i < d; i += 32) out[(size_t)v * d + i] = E[i];
+    }
+    __syncwarp();
+  }
+}
+
+int grid_for(uint64_t work, int nt) {
+  uint64_t g = (work + nt - 1) / nt;
+  return (int)(g > 148 * 64 ? 148 * 64 : (g == 0 ? 1 : g));
+}
+
+}  // namespace
+
+void launch_check_sorted(const uint32_t* d_ids, const float* d_dists, uint32_t n, uint32_t deg,
+                         int* d_flag, cudaStream_t stream) {
+  uint64_t total = (uint64_t)n * deg;
+  if (total == 0) return;
+  check_sorted_kernel<<<grid_for(total, 256), 256, 0, stream>>>(d_ids, d_dists, n, deg, d_flag);
+  CAGRA_LAUNCH_CHECK();
+}
+
+void launch_check_ids(const uint32_t* d_ids, uint64_t count, uint32_t n, int* d_flag,
+                      cudaStream_t stream) {
+  if (count == 0) return;
+  check_ids_kernel<<<grid_for(count, 256), 256, 0, stream>>>(d_ids, count, n, d_flag);
+  CAGRA_LAUNCH_CHECK();
+}
+
+static void detour_launch(const uint32_t* d_knn, const uint32_t* d_counts_in, uint32_t n,
+                          uint32_t deg, uint32_t d, uint32_t* d_counts_out,
+                          uint32_t* d_pruned_out, cudaStream_t stream) {
+  uint32_t H = next_pow2_u32(2 * deg);
+  uint32_t P = next_pow2_u32(deg);
+  size_t smem = detour_smem(deg, H, P);
+  if (smem > 200 * 1024) throw UsageErr("optimize: input degree too large for the device kernel");
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(detour_reorder_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = (int)(n < 148u * 64u ? n : 148u * 64u);
+  detour_reorder_kernel<<<grid, OPT_NT, smem, stream>>>(d_knn, n, deg, d, H, P, d_counts_in,
+                                                        d_counts_out, d_pruned_out);
+  CAGRA_LAUNCH_CHECK();
+}
+
+void launch_detour_reorder(const uint32_t* d_knn, uint32_t n, uint32_t deg, uint32_t d,
+                           uint32_t* d_counts_out, uint32_t* d_pruned_out, cudaStream_t stream) {
+  detour_launch(d_knn, nullptr, n, deg, d, d_counts_out, d_pruned_out, stream);
+}
+
+void launch_reorder_from_counts(const uint32_t* d_knn, const uint32_t* d_counts, uint32_t n,
+                                uint32_t deg, uint32_t d, uint32_t* d_pruned_out,
+                                cudaStream_t stream) {
+  detour_launch(d_knn, d_counts, n, deg, d, nullptr, d_pruned_out, stream);
+}
+
+size_t reverse_scratch_bytes(uint32_t n, uint32_t d) {
+  size_t nb = (n + SCAN_TILE - 1) / SCAN_TILE + 1;
+  return 256 + sizeof(uint32_t) * (size_t)n + 256 + sizeof(unsigned long long) * ((size_t)n + 1) +
+         256 + sizeof(uint32_t) * (size_t)n + 256 + sizeof(uint64_t) * (size_t)n * d + 256 +
+         sizeof(unsigned long long) * nb + 256;
+}
+
+static char* carve(char*& p, size_t bytes) {
+  char* r = p;
+  p += (bytes + 255) / 256 * 256;
+  return r;
+}
+
+void launch_reverse(const uint32_t* d_pruned, uint32_t n, uint32_t d, uint32_t cap,
+                    void* d_scratch, uint32_t* d_rev_counts, uint32_t* d_rev_ids,
+                    cudaStream_t stream) {
+  if (cap > 512) throw UsageErr("build_reverse_graph: cap > 512 unsupported on device");
+  char* p = reinterpret_cast<char*>(d_scratch);
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) / 256 * 256);
+  uint32_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  uint32_t* indeg = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * n));
+  auto* start = reinterpret_cast<unsigned long long*>(carve(p, sizeof(unsigned long long) * (n + 1)));
+  uint32_t* fill = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * n));
+  uint64_t* keys = reinterpret_cast<uint64_t*>(carve(p, sizeof(uint64_t) * (size_t)n * d));
+  auto* bsums = reinterpret_cast<unsigned long long*>(carve(p, sizeof(unsigned long long) * (nb + 1)));
+  uint64_t edges = (uint64_t)n * d;
+  CAGRA_CUDA_TRY(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * n, stream));
+  CAGRA_CUDA_TRY(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * n, stream));
+  indeg_kernel<<<grid_for(edges, 256), 256, 0, stream>>>(d_pruned, edges, indeg);
+  CAGRA_LAUNCH_CHECK();
+  scan_partial_kernel<<<nb, SCAN_NT, 0, stream>>>(indeg, n, bsums);
+  CAGRA_LAUNCH_CHECK();
+  scan_block_sums_kernel<<<1, SCAN_NT, 0, stream>>>(bsums, nb);
+  CAGRA_LAUNCH_CHECK();
+  scan_final_kernel<<<nb, SCAN_NT, 0, stream>>>(indeg, n, bsums, start);
+  CAGRA_LAUNCH_CHECK();
+  set_total_kernel<<<1, 1, 0, stream>>>(indeg, n, start);
+  CAGRA_LAUNCH_CHECK();
+  reverse_scatter_kernel<<<grid_for(edges, 256), 256, 0, stream>>>(d_pruned, n, d, start, fill,
+                                                                   keys);
+  CAGRA_LAUNCH_CHECK();
+  size_t smem = sizeof(uint64_t) * REV_BUF * REV_WARPS;
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(reverse_select_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = (int)std::min<uint64_t>((n + REV_WARPS - 1) / REV_WARPS, 148ull * 16);
+  reverse_select_kernel<<<grid, REV_WARPS * 32, smem, stream>>>(start, keys, n, cap,
+                                                                d_rev_counts, d_rev_ids);
+  CAGRA_LAUNCH_CHECK();
+}
+
+void launch_merge(const uint32_t* d_pruned, const uint32_t* d_rev_counts,
+                  const uint32_t* d_rev_ids, uint32_t n, uint32_t d, uint32_t rev_cap,
+                  uint32_t* d_out, int* d_flag, cudaStream_t stream) {
+  size_t smem = sizeof(uint32_t) * (2 * d + rev_cap) * MRG_WARPS;
+  if (smem > 200 * 1024) throw UsageErr("merge_graphs: degree too large for the device kernel");
+  CAGRA_CUDA_TRY(
+      cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = (int)std::min<uint64_t>((n + MRG_WARPS - 1) / MRG_WARPS, 148ull * 32);
+  merge_kernel<<<grid, MRG_WARPS * 32, smem, stream>>>(d_pruned, d_rev_counts, d_rev_ids, n, d,
+                                                       rev_cap, d_out, d_flag);
+  CAGRA_LAUNCH_CHECK();
+}
+
+}  // namespace cagra

@@ -1,0 +1,96 @@
+// Internal launcher declarations shared by the kernel files and capi.cu.
+// Everything here takes DEVICE pointers and is asynchronous on `stream`.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace cagra {
+
+// ---- knn_exact.cu -----------------------------------------------------------
+// Exact top-K by (dist, id) for nq query rows against n data rows (row
+// strides ld / qld floats).  exclude_self drops data index == query index
+// (the kNN graph, knn_build.cpp:52-60).  d_topk_scratch: nq*K u64.
+void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
+                       uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
+                       uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
+                       cudaStream_t stream);
+
+// ---- graph_opt.cu -----------------------------------------------------------
+struct OptTimes {
+  float count_ms = 0, reorder_ms = 0, reverse_ms = 0, merge_ms = 0, total_ms = 0;
+};
+
+// Validation passes (flags are device ints, set non-zero on violation).
+void launch_check_sorted(const uint32_t* d_ids, const float* d_dists, uint32_t n, uint32_t deg,
+                         int* d_flag, cudaStream_t stream);
+void launch_check_ids(const uint32_t* d_ids, uint64_t count, uint32_t n, int* d_flag,
+                      cudaStream_t stream);
+
+// K2: rank-mode detour counting fused with the stable (count, rank) reorder.
+// counts_out (n*deg) and/or pruned_out (n*d) may be null.
+void launch_detour_reorder(const uint32_t* d_knn, uint32_t n, uint32_t deg, uint32_t d,
+                           uint32_t* d_counts_out, uint32_t* d_pruned_out,
+                           cudaStream_t stream);
+// reorder only, from given counts (reorder_and_prune)
+void launch_reorder_from_counts(const uint32_t* d_knn, const uint32_t* d_counts, uint32_t n,
+                                uint32_t deg, uint32_t d, uint32_t* d_pruned_out,
+                                cudaStream_t stream);
+// K3: reverse graph in [n][cap] form + counts.
+struct ReverseScratch {
+  uint32_t* indeg = nullptr;       // n
+  unsigned long long* start = nullptr;  // n+1
+  uint32_t* fill = nullptr;        // n
+  uint64_t* keys = nullptr;        // n*d
+  unsigned long long* block_sums = nullptr;
+};
+size_t reverse_scratch_bytes(uint32_t n, uint32_t d);
+void launch_reverse(const uint32_t* d_pruned, uint32_t n, uint32_t d, uint32_t cap,
+                    void* d_scratch, uint32_t* d_rev_counts, uint32_t* d_rev_ids,
+                    cudaStream_t stream);
+// K4: interleave merge. d_flag set when a row lacks d distinct candidates.
+void launch_merge(const uint32_t* d_pruned, const uint32_t* d_rev_counts,
+                  const uint32_t* d_rev_ids, uint32_t n, uint32_t d, uint32_t rev_cap,
+                  uint32_t* d_out, int* d_flag, cudaStream_t stream);
+
+// ---- search.cu ----------------------------------------------------------------
+struct SearchConfig {
+  uint32_t k, topm, width, max_iter, min_iter, hash_policy, hash_bits, reset_interval;
+  uint64_t seed;
+  uint32_t mode, team_count, seed_mode, exact, team_size;
+  uint64_t query_offset;
+};
+
+struct DeviceIndexView {
+  const float* data;   // n x ld
+  const uint32_t* graph;  // n x degree
+  uint32_t n, dim, ld, degree;
+};
+
+struct SearchPlan {
+  uint32_t grid = 0, hcap = 0, teams = 1, C = 0, max_iter = 0, min_iter = 0;
+  bool smem_table = false;
+  size_t smem = 0;
+  size_t table_elems = 0;  // u64 slots of HBM visited tables (grid * hcap)
+  size_t init_elems = 0;   // u32 init sample ids
+  const void* fn = nullptr;
+};
+// Validates device limits and picks the kernel variant / grid.
+SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_t nq,
+                       int sm_count, size_t table_budget_bytes);
+// Launches init-sample + search kernels; returns the number of kernels.
+// d_tables / d_gens persist across calls (zeroed when first allocated).
+uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const SearchPlan& pl,
+                       const float* d_queries, uint32_t nq, uint32_t* d_ids, float* d_dists,
+                       uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
+                       uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
+                       cudaStream_t stream);
+
+// ---- merge.cu (K8) --------------------------------------------------------------
+void launch_shard_merge(const uint32_t* d_shard_ids, const float* d_shard_dists,
+                        uint32_t shards, uint32_t nq, uint32_t k, const uint64_t* d_offsets,
+                        uint32_t* d_ids, float* d_dists, cudaStream_t stream);
+
+}  // namespace cagra

@@ -1,0 +1,1201 @@
+// Batch beam search on device — the north-star hot path.
+//
+//   search_one / Traversal (search.cpp:147-268) and batch_search
+//   (engine.cpp:95-120), per-query mode: ONE CTA PER QUERY (persistent CTAs
+//   pull queries from an atomic counter).
+//   shared_query_search (engine.cpp:38-78): T lockstep teams inside one CTA
+//   sharing one visited table, reproducing the reference's team order.
+//
+// Per query, shared memory holds the query, the sorted top-M list (double
+// buffered), the candidate "survivors" of the last expansion and, for the
+// forgettable policy, the open-addressing visited table.  The standard
+// policy's visited set lives in a generation-tagged table in HBM (one region
+// per resident CTA, never cleared: a bumped tag empties it).
+//
+// Reference semantics reproduced exactly (ids, distances, counters):
+//   * buffer order (dist, stripped id) with flag-OR dedup — entries are 64-bit
+//     keys (dist bits << 32 | id), see common.cuh;
+//   * update_topm (search.cpp:55-85) == merge of the previous expansion's
+//     candidates into top-M.  Candidates that cannot enter top-M (key >= the
+//     M-th key) are dropped at expansion time ("survivors" only), duplicates
+//     of top-M entries are dropped (equivalent to the flag-OR collapse, the
+//     top-M copy already carries the flag);
+//   * select_parents (search.cpp:87-98): first p unflagged non-dummy entries;
+//   * visited semantics, including forgettable "Full" early resets in exact
+//     reference order (serial slow path when an expansion could fill the table);
+//   * init samples: state = mix_seed(qseed ^ 0x5eed), id = mix_seed-chain % N
+//     (search.cpp:163, 192-201), precomputed by init_samples_kernel;
+//   * termination / convergence / I_max (search.cpp:218-245) and finish
+//     (:247-259).
+// Distances: EXACT=true uses the sequential fp32 chain of squared_l2 per
+// candidate (bit-equal to the CPU).  EXACT=false ("fast") splits a row over a
+// team of lanes with 128-bit loads and a shuffle reduction; the final k are
+// re-scored with the sequential chain and re-sorted, so reported distances are
+// always bit-equal to the reference's.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cagra {
+namespace {
+
+constexpr int SNT = 256;  // threads per search CTA
+constexpr int SWARPS = SNT / 32;
+
+struct DevStats {
+  uint32_t iterations, hash_resets;
+  unsigned long long distance_evals;
+  uint32_t converged, pad;
+};
+
+struct KParams {
+  const float* data;
+  const uint32_t* graph;
+  uint32_t n, dim, ld, degree;
+  const float* queries;
+  uint32_t nq;
+  uint32_t k, M, p, C, max_iter, min_iter, policy, reset_interval;
+  uint32_t hcap;  // visited capacity (power of two)
+  uint32_t teams;  // shared mode team count (1 for per-query)
+  const uint32_t* init_ids;  // [nq][teams*C]
+  unsigned long long* gtables;  // [grid][hcap] when the table is global
+  uint32_t* gens;               // [grid]
+  uint32_t* work;               // query counter
+  uint32_t* out_ids;
+  float* out_dists;
+  uint32_t* out_counts;
+  DevStats* stats;
+  int* error;
+};
+
+// ------------------------------------------------------------- init ids ----
+__global__ void init_samples_kernel(uint32_t nq, uint32_t C, uint32_t teams, uint32_t n,
+                                    uint64_t seed, uint32_t seed_mode, uint64_t qoff,
+                                    uint32_t* __restrict__ out) {
+  uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t t = blockIdx.y;
+  if (qi >= nq) return;
+  // engine.cpp:108 / search.cpp:163 / engine.cpp:56
+  uint64_t qseed = seed_mode == 0 ? mix_seed(seed ^ (0x0badull + qoff + qi)) : seed;
+  uint64_t tseed = teams > 1 ? mix_seed(qseed + 0x7ea4ull * (t + 1)) : qseed;
+  uint64_t state = mix_seed(tseed ^ 0x5eedull);
+  uint32_t* o = out + ((size_t)qi * teams + t) * C;
+  for (uint32_t j = 0; j < C; ++j) {
+    state = mix_seed(state);
+    o[j] = (uint32_t)(state % n);
+  }
+}
+
+// ------------------------------------------------------------ sorting ------
+// Bitonic sort of 32*E keys held blocked in registers (index = lane*E + e).
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[E], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            int i = lane * E + e;
+            bool up = (i & k) == 0;
+            uint64_t a = v[e], b = v[e ^ j];
+            if ((a > b) == up) {
+              v[e] = b;
+              v[e ^ j] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          int i = lane * E + e;
+          uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+          bool up = (i & k) == 0;
+          bool lower = (i & j) == 0;
+          uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_smem_E(uint64_t* a, uint32_t cnt, int lane) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    uint32_t i = lane * E + e;
+    v[e] = i < cnt ? a[i] : kDummyKey;
+  }
+  warp_sort_regs<E>(v, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    uint32_t i = lane * E + e;
+    if (i < cnt) a[i] = v[e];
+  }
+}
+
+// Sort a[0..cnt) ascending using one warp (cnt <= 256).
+__device__ __noinline__ void warp_sort_smem(uint64_t* a, uint32_t cnt, int lane) {
+  if (cnt <= 1) return;
+  if (cnt <= 32) warp_sort_smem_E<1>(a, cnt, lane);
+  else if (cnt <= 64) warp_sort_smem_E<2>(a, cnt, lane);
+  else if (cnt <= 128) warp_sort_smem_E<4>(a, cnt, lane);
+  else warp_sort_smem_E<8>(a, cnt, lane);
+  __syncwarp();
+}
+
+// Block-wide bitonic sort of a[0..P), P power of two (caller syncs before).
+__device__ void block_sort_smem(uint64_t* a, uint32_t P) {
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          uint64_t x = a[i], y = a[ixj];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// #{i < len : cmp_key(a[i]) < key}   (a sorted by cmp_key)
+__device__ __forceinline__ uint32_t lb_cmp(const uint64_t* a, uint32_t len, uint64_t key) {
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (cmp_key(a[mid]) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------ visited -----
+// Shared-memory table: u32 slots, kInvalidId = empty.
+__device__ __forceinline__ bool smem_insert(uint32_t* tab, uint32_t mask, uint32_t id) {
+  uint32_t h = hash_id(id, mask);
+  for (;;) {
+    uint32_t old = atomicCAS(&tab[h], kInvalidId, id);
+    if (old == kInvalidId) return true;
+    if (old == id) return false;
+    h = (h + 1) & mask;
+  }
+}
+
+// HBM table: u64 slots (tag << 32 | id); a slot whose tag differs from the
+// current generation is empty.
+__device__ __forceinline__ bool gtab_insert(unsigned long long* tab, uint32_t mask, uint32_t tag,
+                                            uint32_t id) {
+  const unsigned long long want = ((unsigned long long)tag << 32) | id;
+  uint32_t h = hash_id(id, mask);
+  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&tab[h]);
+  for (;;) {
+    if ((uint32_t)(cur >> 32) != tag) {
+      unsigned long long old = atomicCAS(&tab[h], cur, want);
+      if (old == cur) return true;
+      cur = old;  // re-examine the same slot
+      continue;
+    }
+    if ((uint32_t)cur == id) return false;
+    h = (h + 1) & mask;
+    cur = *reinterpret_cast<volatile unsigned long long*>(&tab[h]);
+  }
+}
+
+// ------------------------------------------------------------ distances ----
+__device__ __forceinline__ float exact_dist(const float* __restrict__ row, const float* q,
+                                            uint32_t dim) {
+  float acc = 0.0f;
+  uint32_t i = 0;
+  for (; i + 4 <= dim; i += 4) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(row + i));
+    acc = seq_step(acc, x.x, q[i]);
+    acc = seq_step(acc, x.y, q[i + 1]);
+    acc = seq_step(acc, x.z, q[i + 2]);
+    acc = seq_step(acc, x.w, q[i + 3]);
+  }
+  for (; i < dim; ++i) acc = seq_step(acc, __ldg(row + i), q[i]);
+  return acc;
+}
+
+// ------------------------------------------------------------- the CTA -----
+// All per-query state of the CTA, carved from dynamic shared memory.
+struct Smem {
+  float* q;            // ld
+  uint64_t* topA;      // teams * M
+  uint64_t* topB;      // teams * M
+  uint64_t* surv;      // teams * SP
+  uint32_t* evlist;    // teams * C   (ids to evaluate)
+  uint16_t* evteam;    // teams * C   (owning team of each evlist entry)
+  uint32_t* parents;   // teams * p
+  uint32_t* table;     // hcap (smem table only)
+  uint32_t* rclaim;    // shared mode: round first-occurrence hash (RP ids + RP orders)
+  uint32_t* cand;      // shared mode: the round's candidates in reference order
+  uint64_t* fin;       // shared mode: merged team results
+};
+
+struct Ctl {
+  uint32_t qi, nev, npar_total, count, dup, slow;
+  uint32_t nsurv[16];
+  uint32_t npar[16];
+  uint32_t warp_cnt[SWARPS];
+  uint64_t worst[16];
+  uint32_t iters[16];
+  uint32_t done[16];
+  uint32_t conv[16];
+  unsigned long long evals[16];
+  uint32_t resets;
+  uint32_t pending[16];
+};
+
+template <int TEAM, int MAXC, bool EXACT>
+__device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& ctl,
+                                          uint32_t nev, uint32_t SP) {
+  const int tid = threadIdx.x;
+  if (EXACT) {
+    for (uint32_t e = tid; e < nev; e += SNT) {
+      uint32_t id = S.evlist[e];
+      uint32_t t = S.evteam[e];
+      float dist = exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim);
+      uint64_t key = make_key(dist, id);
+      if (key < ctl.worst[t]) {
+        uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
+        S.surv[t * SP + pos] = key;
+      }
+    }
+  } else {
+    constexpr int NTEAMS = SNT / TEAM;
+    const int team = tid / TEAM, lt = tid % TEAM;
+    const uint32_t nchunk = P.ld >> 2;
+    float4 qr[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      uint32_t ch = lt + TEAM * c;
+      qr[c] = ch < nchunk ? reinterpret_cast<const float4*>(S.q)[ch] : make_float4(0, 0, 0, 0);
+    }
+    constexpr int U = 2;  // rows in flight per team
+    for (uint32_t e0 = team; e0 < nev; e0 += NTEAMS * U) {
+      float4 xv[U][MAXC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t e = e0 + u * NTEAMS;
+        uint32_t id = e < nev ? S.evlist[e] : 0;
+        const float4* row = reinterpret_cast<const float4*>(P.data + (size_t)id * P.ld);
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          uint32_t ch = lt + TEAM * c;
+          xv[u][c] = (e < nev && ch < nchunk) ? __ldg(row + ch) : make_float4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          float dx = xv[u][c].x - qr[c].x, dy = xv[u][c].y - qr[c].y;
+          float dz = xv[u][c].z - qr[c].z, dw = xv[u][c].w - qr[c].w;
+          acc = fmaf(dx, dx, acc);
+          acc = fmaf(dy, dy, acc);
+          acc = fmaf(dz, dz, acc);
+          acc = fmaf(dw, dw, acc);
+        }
+#pragma unroll
+        for (int o = TEAM / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        uint32_t e = e0 + u * NTEAMS;
+        if (lt == 0 && e < nev) {
+          uint32_t id = S.evlist[e];
+          uint32_t t = S.evteam[e];
+          uint64_t key = make_key(acc, id);
+          if (key < ctl.worst[t]) {
+            uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
+            S.surv[t * SP + pos] = key;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Generic (any dimension) fast path: query read from shared memory.
+template <bool EXACT>
+__device__ __forceinline__ void eval_list_generic(const KParams& P, const Smem& S, Ctl& ctl,
+                                                  uint32_t nev, uint32_t SP) {
+  if (EXACT) {
+    eval_list<32, 1, true>(P, S, ctl, nev, SP);
+    return;
+  }
+  const int tid = threadIdx.x, team = tid / 32, lt = tid % 32;
+  const uint32_t nchunk = P.ld >> 2;
+  for (uint32_t e = team; e < nev; e += SWARPS) {
+    uint32_t id = S.evlist[e];
+    const float4* row = reinterpret_cast<const float4*>(P.data + (size_t)id * P.ld);
+    float acc = 0.0f;
+    for (uint32_t ch = lt; ch < nchunk; ch += 32) {
+      float4 x = __ldg(row + ch), q = reinterpret_cast<const float4*>(S.q)[ch];
+      float dx = x.x - q.x, dy = x.y - q.y, dz = x.z - q.z, dw = x.w - q.w;
+      acc = fmaf(dx, dx, acc);
+      acc = fmaf(dy, dy, acc);
+      acc = fmaf(dz, dz, acc);
+      acc = fmaf(dw, dw, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lt == 0) {
+      uint32_t t = S.evteam[e];
+      uint64_t key = make_key(acc, id);
+      if (key < ctl.worst[t]) {
+        uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
+        S.surv[t * SP + pos] = key;
+      }
+    }
+  }
+}
+
+// Visited-table reset with the current top-M ids (reset_table,
+// search.cpp:138-145).  Called by all threads; top-M ids are distinct, so the
+// parallel inserts fill exactly the first min(live, hcap) entries.
+template <bool SMEM_TABLE>
+__device__ void table_reset(const KParams& P, const Smem& S, Ctl& ctl, const uint64_t* top,
+                            unsigned long long* gtab, uint32_t& tag) {
+  if (SMEM_TABLE) {
+    for (uint32_t i = threadIdx.x; i < P.hcap; i += SNT) S.table[i] = kInvalidId;
+  } else {
+    tag = tag + 1;  // every thread keeps the same register copy
+  }
+  __syncthreads();
+  uint32_t live = 0;
+  {
+    // dummies form the tail of the sorted list
+    uint32_t lo = 0, hi = P.M;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (!key_is_dummy(top[mid])) lo = mid + 1;
+      else hi = mid;
+    }
+    live = lo;
+  }
+  uint32_t lim = live < P.hcap ? live : P.hcap;
+  for (uint32_t i = threadIdx.x; i < lim; i += SNT) {
+    uint32_t id = key_id(top[i]) & kIdMask;
+    if (SMEM_TABLE) smem_insert(S.table, P.hcap - 1, id);
+    else gtab_insert(gtab, P.hcap - 1, tag, id);
+  }
+  if (threadIdx.x == 0) ctl.count = lim;
+  __syncthreads();
+}
+
+// Serial (reference-order) visited processing of candidates when the
+// forgettable table could fill mid-expansion (eval_or_skip, search.cpp:168-190).
+template <bool SMEM_TABLE>
+__device__ void serial_visit(const KParams& P, const Smem& S, Ctl& ctl, const uint32_t* ids,
+                             uint32_t cnt, const uint64_t* top, unsigned long long* gtab,
+                             uint32_t& tag) {
+  // thread 0 only; tag is advanced in ctl via return (caller broadcasts)
+  const uint32_t mask = P.hcap - 1;
+  auto ins = [&](uint32_t id) -> int {  // 0 new, 1 present, 2 full
+    if (ctl.count == P.hcap) return 2;
+    uint32_t h = hash_id(id, mask);
+    for (;;) {
+      if (SMEM_TABLE) {
+        uint32_t s = S.table[h];
+        if (s == kInvalidId) {
+          S.table[h] = id;
+          break;
+        }
+        if (s == id) return 1;
+      } else {
+        unsigned long long s = gtab[h];
+        if ((uint32_t)(s >> 32) != tag) {
+          gtab[h] = ((unsigned long long)tag << 32) | id;
+          break;
+        }
+        if ((uint32_t)s == id) return 1;
+      }
+      h = (h + 1) & mask;
+    }
+    ctl.count++;
+    return 0;
+  };
+  auto reset = [&]() {
+    if (SMEM_TABLE) {
+      for (uint32_t i = 0; i < P.hcap; ++i) S.table[i] = kInvalidId;
+    } else {
+      tag = tag + 1;
+    }
+    ctl.count = 0;
+    for (uint32_t i = 0; i < P.M; ++i) {
+      if (key_is_dummy(top[i])) break;
+      ins(key_id(top[i]) & kIdMask);
+    }
+  };
+  uint32_t nev = 0;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    uint32_t id = ids[j];
+    int r = ins(id);
+    if (r == 2) {
+      reset();
+      ctl.resets++;
+      r = ins(id);
+    }
+    if (r == 0) {
+      S.evlist[nev] = id;
+      S.evteam[nev] = 0;
+      ++nev;
+    }
+  }
+  ctl.nev = nev;
+}
+
+// ------------------------------------------------------ per-query kernel ---
+template <int TEAM, int MAXC, bool EXACT, bool SMEM_TABLE>
+__global__ void __launch_bounds__(SNT)
+search_kernel(const KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctl ctl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t SP = next_pow2_u32(P.C);
+  Smem S;
+  {
+    unsigned char* p = smem_raw;
+    S.q = reinterpret_cast<float*>(p);
+    p += sizeof(float) * round_up_u32(P.ld, 4);
+    S.topA = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * P.M;
+    S.topB = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * P.M;
+    S.surv = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * SP;
+    S.evlist = reinterpret_cast<uint32_t*>(p);
+    p += sizeof(uint32_t) * P.C;
+    S.evteam = reinterpret_cast<uint16_t*>(p);
+    p += sizeof(uint16_t) * round_up_u32(P.C, 2);
+    S.parents = reinterpret_cast<uint32_t*>(p);
+    p += sizeof(uint32_t) * round_up_u32(P.p, 4);
+    S.table = reinterpret_cast<uint32_t*>(p);
+  }
+  unsigned long long* gtab = SMEM_TABLE ? nullptr : P.gtables + (size_t)blockIdx.x * P.hcap;
+  uint32_t tag = SMEM_TABLE ? 0 : P.gens[blockIdx.x];
+  const uint32_t mask = P.hcap - 1;
+  const bool forget = P.policy == 1;
+
+  for (;;) {
+    if (tid == 0) ctl.qi = atomicAdd(P.work, 1u);
+    __syncthreads();
+    const uint32_t qi = ctl.qi;
+    if (qi >= P.nq) break;
+    // ---- per-query setup
+    for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qi * P.ld + i];
+    for (uint32_t i = tid; i < P.M; i += SNT) S.topA[i] = kDummyKey;
+    if (SMEM_TABLE)
+      for (uint32_t i = tid; i < P.hcap; i += SNT) S.table[i] = kInvalidId;
+    tag = tag + 1;
+    if (tid == 0) {
+      ctl.nsurv[0] = 0;
+      ctl.count = 0;
+      ctl.resets = 0;
+      ctl.evals[0] = 0;
+      ctl.iters[0] = 0;
+      ctl.conv[0] = 0;
+      ctl.worst[0] = kDummyKey;
+      ctl.dup = 0;
+    }
+    __syncthreads();
+
+    uint64_t* top = S.topA;
+    uint64_t* nxt = S.topB;
+    const uint32_t* init = P.init_ids + (size_t)qi * P.C;
+
+    // visit(): candidates [src 0..cnt) -> evlist of first visits
+    auto visit = [&](const uint32_t* src_ids, bool from_graph, uint32_t cnt) {
+      bool slow = forget && (ctl.count + cnt > P.hcap);
+      if (!slow) {
+        if (tid == 0) ctl.nev = 0;
+        __syncthreads();
+        for (uint32_t j = tid; j < cnt; j += SNT) {
+          uint32_t id;
+          if (from_graph) {
+            uint32_t pi = j / P.degree, c = j - pi * P.degree;
+            id = __ldg(&P.graph[(size_t)S.parents[pi] * P.degree + c]);
+          } else {
+            id = __ldg(&src_ids[j]);
+          }
+          bool ins = SMEM_TABLE ? smem_insert(S.table, mask, id) : gtab_insert(gtab, mask, tag, id);
+          if (ins) {
+            uint32_t pos = atomicAdd(&ctl.nev, 1u);
+            S.evlist[pos] = id;
+            S.evteam[pos] = 0;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) ctl.count += ctl.nev;
+      } else {
+        // materialise candidate ids in reference order, then serial visit
+        for (uint32_t j = tid; j < cnt; j += SNT) {
+          uint32_t id;
+          if (from_graph) {
+            uint32_t pi = j / P.degree, c = j - pi * P.degree;
+            id = P.graph[(size_t)S.parents[pi] * P.degree + c];
+          } else {
+            id = src_ids[j];
+          }
+          reinterpret_cast<uint32_t*>(S.surv)[j] = id;  // scratch (survivors are empty now)
+        }
+        __syncthreads();
+        if (tid == 0) {
+          uint32_t t2 = tag;
+          serial_visit<SMEM_TABLE>(P, S, ctl, reinterpret_cast<uint32_t*>(S.surv), cnt, top,
+                                   gtab, t2);
+          ctl.slow = t2;
+          ctl.dup = 1;
+        }
+        __syncthreads();
+        if (!SMEM_TABLE) tag = ctl.slow;
+      }
+      __syncthreads();
+      uint32_t nev = ctl.nev;
+      if (MAXC > 0) eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT>(P, S, ctl, nev, SP);
+      else eval_list_generic<EXACT>(P, S, ctl, nev, SP);
+      if (tid == 0) ctl.evals[0] += nev;
+      __syncthreads();
+    };
+
+    // update_topm(): merge survivors into top
+    auto merge = [&]() {
+      uint32_t ns = ctl.nsurv[0];
+      if (ns > 0) {
+        // drop duplicates of top-M entries (forgettable revisits)
+        if (forget) {
+          for (uint32_t j = tid; j < ns; j += SNT) {
+            uint64_t s = S.surv[j];
+            uint32_t ix = lb_cmp(top, P.M, s);
+            if (ix < P.M && cmp_key(top[ix]) == s) S.surv[j] = kDummyKey;
+          }
+          __syncthreads();
+        }
+        if (ns <= 256) {
+          if (warp == 0) warp_sort_smem(S.surv, ns, lane);
+        } else {
+          uint32_t P2 = next_pow2_u32(ns);
+          for (uint32_t j = ns + tid; j < P2; j += SNT) S.surv[j] = kDummyKey;
+          __syncthreads();
+          block_sort_smem(S.surv, P2);
+        }
+        __syncthreads();
+        if (ctl.dup) {
+          // a serial visit may admit one id twice: collapse adjacent equals
+          __syncthreads();
+          if (tid == 0) {
+            uint32_t w = 0;
+            for (uint32_t j = 0; j < ns; ++j) {
+              uint64_t s = S.surv[j];
+              if (key_is_dummy(s)) break;
+              if (w > 0 && S.surv[w - 1] == s) continue;
+              S.surv[w++] = s;
+            }
+            ctl.nsurv[0] = w;
+            ctl.dup = 0;
+          }
+          __syncthreads();
+          ns = ctl.nsurv[0];
+        } else if (forget) {
+          // count survivors that are not dummies (dummies sorted last)
+          uint32_t lo = 0, hi = ns;
+          while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (!key_is_dummy(S.surv[mid])) lo = mid + 1;
+            else hi = mid;
+          }
+          ns = lo;
+        }
+        for (uint32_t i = tid; i < P.M; i += SNT) {
+          uint64_t e = top[i];
+          uint32_t lo = 0, hi = ns;
+          uint64_t ke = cmp_key(e);
+          while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (S.surv[mid] < ke) lo = mid + 1;
+            else hi = mid;
+          }
+          uint32_t pos = i + lo;
+          if (pos < P.M) nxt[pos] = e;
+        }
+        for (uint32_t j = tid; j < ns; j += SNT) {
+          uint64_t s = S.surv[j];
+          uint32_t pos = j + lb_cmp(top, P.M, s);
+          if (pos < P.M) nxt[pos] = s;
+        }
+        __syncthreads();
+        uint64_t* t = top;
+        top = nxt;
+        nxt = t;
+        if (tid == 0) ctl.nsurv[0] = 0;
+      }
+      __syncthreads();
+    };
+
+    // ---- init (search.cpp:192-201)
+    visit(init, false, P.C);
+    bool pending = true;
+    uint32_t iters = 0;
+    bool converged = false;
+    for (;;) {
+      // ---- step (search.cpp:218-245)
+      merge();
+      pending = false;
+      ++iters;
+      // select_parents: first p unflagged non-dummy entries
+      if (tid == 0) ctl.npar[0] = 0;
+      __syncthreads();
+      for (uint32_t c0 = 0; c0 < P.M; c0 += SNT) {
+        uint32_t have = ctl.npar[0];
+        if (have >= P.p) break;
+        uint32_t i = c0 + tid;
+        uint64_t e = i < P.M ? top[i] : kDummyKey;
+        bool elig = i < P.M && !key_is_dummy(e) && !(e & kFlagBit64);
+        unsigned bal = __ballot_sync(0xffffffffu, elig);
+        if (lane == 0) ctl.warp_cnt[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+        for (int w = 0; w < SWARPS; ++w) {
+          uint32_t c = ctl.warp_cnt[w];
+          if (w < warp) off += c;
+          tot += c;
+        }
+        uint32_t rank = have + off + __popc(bal & ((1u << lane) - 1));
+        if (elig && rank < P.p) {
+          S.parents[rank] = key_id(e) & kIdMask;
+          top[i] = e | kFlagBit64;
+        }
+        __syncthreads();
+        if (tid == 0) ctl.npar[0] = min(P.p, have + tot);
+        __syncthreads();
+      }
+      uint32_t np = ctl.npar[0];
+      if (np == 0) {
+        converged = iters >= P.min_iter;
+        break;
+      }
+      // worst key of top-M bounds which candidates can matter
+      if (tid == 0) ctl.worst[0] = cmp_key(top[P.M - 1]);
+      __syncthreads();
+      visit(nullptr, true, np * P.degree);
+      pending = true;
+      if (forget && iters % P.reset_interval == 0) {
+        table_reset<SMEM_TABLE>(P, S, ctl, top, gtab, tag);
+        if (tid == 0) ctl.resets++;
+      }
+      if (iters >= P.max_iter) break;
+    }
+    if (pending) merge();
+
+    // ---- finish (search.cpp:247-259)
+    uint32_t live;
+    {
+      uint32_t lo = 0, hi = P.k;
+      while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (!key_is_dummy(top[mid])) lo = mid + 1;
+        else hi = mid;
+      }
+      live = lo;
+    }
+    if (!EXACT) {
+      // re-score the final k with the sequential chain, re-sort by (dist, id)
+      for (uint32_t i = tid; i < live; i += SNT) {
+        uint32_t id = key_id(top[i]) & kIdMask;
+        nxt[i] = make_key(exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim), id);
+      }
+      __syncthreads();
+      if (live <= 256) {
+        if (warp == 0) warp_sort_smem(nxt, live, lane);
+      } else {
+        uint32_t P2 = next_pow2_u32(live);
+        for (uint32_t j = live + tid; j < P2; j += SNT) nxt[j] = kDummyKey;
+        __syncthreads();
+        block_sort_smem(nxt, P2);
+      }
+      __syncthreads();
+      top = nxt;
+    }
+    for (uint32_t i = tid; i < P.k; i += SNT) {
+      bool ok = i < live;
+      uint64_t e = ok ? top[i] : kDummyKey;
+      P.out_ids[(size_t)qi * P.k + i] = ok ? (key_id(e) & kIdMask) : kInvalidId;
+      P.out_dists[(size_t)qi * P.k + i] = key_dist(e);
+    }
+    if (tid == 0) {
+      P.out_counts[qi] = live;
+      if (P.stats) {
+        DevStats st;
+        st.iterations = iters;
+        st.hash_resets = ctl.resets;
+        st.distance_evals = ctl.evals[0];
+        st.converged = converged ? 1u : 0u;
+        st.pad = 0;
+        P.stats[qi] = st;
+      }
+    }
+    __syncthreads();
+  }
+  if (!SMEM_TABLE && tid == 0) P.gens[blockIdx.x] = tag;
+}
+
+
+// --------------------------------------------------- shared-mode kernel ----
+// shared_query_search (engine.cpp:38-78): T traversals (p = 1, k = M,
+// standard policy) share one visited table and advance in lockstep rounds,
+// team 0 first.  Candidate (t, j) of a round is a first visit iff its id was
+// not visited in an earlier round and no (t', j') < (t, j) of the same round
+// carries the same id — exactly the reference's sequential team order.  Team
+// merges / parent selection run one warp per team; expansions of all teams
+// run CTA-wide.
+template <int TEAM, int MAXC, bool EXACT>
+__global__ void __launch_bounds__(SNT)
+shared_search_kernel(const KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctl ctl;
+  __shared__ uint32_t parity;  // bit t: team t's current top list is in topB
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t T = P.teams;
+  const uint32_t d = P.degree;
+  const uint32_t SP = next_pow2_u32(d);
+  const uint32_t RP = next_pow2_u32(2 * T * d);
+  const uint32_t KP = next_pow2_u32(P.k);
+  Smem S;
+  {
+    unsigned char* p = smem_raw;
+    S.q = reinterpret_cast<float*>(p);
+    p += sizeof(float) * round_up_u32(P.ld, 4);
+    S.topA = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * P.M * T;
+    S.topB = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * P.M * T;
+    S.surv = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * SP * T;
+    S.fin = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * KP;
+    S.rclaim = reinterpret_cast<uint32_t*>(p);
+    p += sizeof(uint32_t) * 2 * RP;
+    S.cand = reinterpret_cast<uint32_t*>(p);
+    p += sizeof(uint32_t) * T * d;
+    S.evlist = reinterpret_cast<uint32_t*>(p);
+    p += sizeof(uint32_t) * T * d;
+    S.evteam = reinterpret_cast<uint16_t*>(p);
+    p += sizeof(uint16_t) * round_up_u32(T * d, 2);
+    S.parents = reinterpret_cast<uint32_t*>(p);
+  }
+  unsigned long long* gtab = P.gtables + (size_t)blockIdx.x * P.hcap;
+  uint32_t tag = P.gens[blockIdx.x];
+  const uint32_t mask = P.hcap - 1;
+
+  auto team_top = [&](uint32_t t) -> uint64_t* {
+    return ((parity >> t) & 1u) ? S.topB + t * P.M : S.topA + t * P.M;
+  };
+  auto team_nxt = [&](uint32_t t) -> uint64_t* {
+    return ((parity >> t) & 1u) ? S.topA + t * P.M : S.topB + t * P.M;
+  };
+
+  for (;;) {
+    if (tid == 0) ctl.qi = atomicAdd(P.work, 1u);
+    __syncthreads();
+    const uint32_t qi = ctl.qi;
+    if (qi >= P.nq) break;
+    for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qi * P.ld + i];
+    for (uint32_t i = tid; i < P.M * T; i += SNT) S.topA[i] = kDummyKey;
+    tag = tag + 1;
+    if (tid < (int)T) {
+      ctl.nsurv[tid] = 0;
+      ctl.evals[tid] = 0;
+      ctl.iters[tid] = 0;
+      ctl.done[tid] = 0;
+      ctl.conv[tid] = 0;
+      ctl.worst[tid] = kDummyKey;
+      ctl.npar[tid] = 0;
+      ctl.pending[tid] = 0;
+    }
+    if (tid == 0) parity = 0;
+    __syncthreads();
+
+    // Process one lockstep round of candidates for the teams in `active`.
+    auto round_visit = [&](bool init_phase, uint32_t active) {
+      const uint32_t total = T * d;
+      for (uint32_t i = tid; i < 2 * RP; i += SNT) S.rclaim[i] = kInvalidId;
+      if (tid == 0) ctl.nev = 0;
+      __syncthreads();
+      for (uint32_t o = tid; o < total; o += SNT) {
+        uint32_t t = o / d, j = o - t * d;
+        if (!((active >> t) & 1u)) continue;
+        uint32_t id = init_phase ? __ldg(&P.init_ids[((size_t)qi * T + t) * d + j])
+                                 : __ldg(&P.graph[(size_t)S.parents[t] * d + j]);
+        S.cand[o] = id;
+        uint32_t h = hash_id(id, RP - 1);
+        for (;;) {
+          uint32_t old = atomicCAS(&S.rclaim[h], kInvalidId, id);
+          if (old == kInvalidId || old == id) break;
+          h = (h + 1) & (RP - 1);
+        }
+        atomicMin(&S.rclaim[RP + h], o);
+      }
+      __syncthreads();
+      for (uint32_t o = tid; o < total; o += SNT) {
+        uint32_t t = o / d;
+        if (!((active >> t) & 1u)) continue;
+        uint32_t id = S.cand[o];
+        uint32_t h = hash_id(id, RP - 1);
+        while (S.rclaim[h] != id) h = (h + 1) & (RP - 1);
+        if (S.rclaim[RP + h] == o && gtab_insert(gtab, mask, tag, id)) {
+          uint32_t pos = atomicAdd(&ctl.nev, 1u);
+          S.evlist[pos] = id;
+          S.evteam[pos] = (uint16_t)t;
+          atomicAdd(&ctl.evals[t], 1ull);
+        }
+      }
+      __syncthreads();
+      uint32_t nev = ctl.nev;
+      if (MAXC > 0) eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT>(P, S, ctl, nev, SP);
+      else eval_list_generic<EXACT>(P, S, ctl, nev, SP);
+      __syncthreads();
+    };
+
+    // update_topm of team t by one warp
+    auto team_merge = [&](uint32_t t) {
+      uint32_t ns = ctl.nsurv[t];
+      if (ns == 0) return;
+      uint64_t* top = team_top(t);
+      uint64_t* nxt = team_nxt(t);
+      uint64_t* sv = S.surv + t * SP;
+      warp_sort_smem(sv, ns, lane);
+      for (uint32_t i = lane; i < P.M; i += 32) {
+        uint64_t e = top[i];
+        uint64_t ke = cmp_key(e);
+        uint32_t lo = 0, hi = ns;
+        while (lo < hi) {
+          uint32_t mid = (lo + hi) >> 1;
+          if (sv[mid] < ke) lo = mid + 1;
+          else hi = mid;
+        }
+        uint32_t pos = i + lo;
+        if (pos < P.M) nxt[pos] = e;
+      }
+      for (uint32_t j = lane; j < ns; j += 32) {
+        uint64_t s = sv[j];
+        uint32_t pos = j + lb_cmp(top, P.M, s);
+        if (pos < P.M) nxt[pos] = s;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        atomicXor(&parity, 1u << t);
+        ctl.nsurv[t] = 0;
+      }
+      __syncwarp();
+    };
+
+    // init: every team's d samples, team order (engine.cpp:59)
+    round_visit(true, (1u << T) - 1);
+    if (tid < (int)T) ctl.pending[tid] = 1;
+    __syncthreads();
+    uint32_t live_mask = (1u << T) - 1;
+    while (live_mask) {
+      for (uint32_t t = warp; t < T; t += SWARPS) {
+        if (!((live_mask >> t) & 1u)) continue;
+        team_merge(t);
+        if (lane == 0) {
+          ctl.pending[t] = 0;
+          ctl.iters[t]++;
+        }
+        __syncwarp();
+        uint64_t* top = team_top(t);
+        uint32_t found = kInvalidId;
+        for (uint32_t c0 = 0; c0 < P.M && found == kInvalidId; c0 += 32) {
+          uint32_t i = c0 + lane;
+          uint64_t e = i < P.M ? top[i] : kDummyKey;
+          bool elig = i < P.M && !key_is_dummy(e) && !(e & kFlagBit64);
+          unsigned bal = __ballot_sync(0xffffffffu, elig);
+          if (bal) found = c0 + __ffs(bal) - 1;
+        }
+        if (lane == 0) {
+          if (found == kInvalidId) {
+            ctl.npar[t] = 0;
+            ctl.conv[t] = ctl.iters[t] >= P.min_iter;
+            ctl.done[t] = 1;
+          } else {
+            uint64_t e = top[found];
+            S.parents[t] = key_id(e) & kIdMask;
+            top[found] = e | kFlagBit64;
+            ctl.npar[t] = 1;
+            ctl.worst[t] = cmp_key(top[P.M - 1]);
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      uint32_t expand_mask = 0;
+      for (uint32_t t = 0; t < T; ++t)
+        if (((live_mask >> t) & 1u) && ctl.npar[t]) expand_mask |= 1u << t;
+      if (expand_mask) round_visit(false, expand_mask);
+      if (tid < (int)T && ((expand_mask >> tid) & 1u)) {
+        ctl.pending[tid] = 1;
+        if (ctl.iters[tid] >= P.max_iter) ctl.done[tid] = 1;
+      }
+      __syncthreads();
+      uint32_t nl = 0;
+      for (uint32_t t = 0; t < T; ++t)
+        if (((live_mask >> t) & 1u) && !ctl.done[t]) nl |= 1u << t;
+      live_mask = nl;
+      __syncthreads();
+    }
+    // finish every team (search.cpp:247-259)
+    for (uint32_t t = warp; t < T; t += SWARPS)
+      if (ctl.pending[t]) team_merge(t);
+    __syncthreads();
+    // merge_team_results (engine.cpp:12-36): T-way merge of the sorted team
+    // lists by (dist, id), ids deduplicated, first k.
+    if (tid == 0) {
+      uint32_t idx[16];
+      for (uint32_t t = 0; t < T; ++t) idx[t] = 0;
+      uint32_t w = 0, prev = kInvalidId;
+      while (w < P.k) {
+        uint64_t best = kDummyKey;
+        int bt = -1;
+        for (uint32_t t = 0; t < T; ++t) {
+          if (idx[t] >= P.M) continue;
+          uint64_t v = cmp_key(team_top(t)[idx[t]]);
+          if (key_is_dummy(team_top(t)[idx[t]])) continue;
+          if (bt < 0 || v < best) {
+            best = v;
+            bt = (int)t;
+          }
+        }
+        if (bt < 0) break;
+        idx[bt]++;
+        uint32_t id = key_id(best);
+        if (id == prev) continue;
+        prev = id;
+        S.fin[w++] = best;
+      }
+      ctl.nev = w;
+    }
+    __syncthreads();
+    const uint32_t live = ctl.nev;
+    if (!EXACT) {
+      for (uint32_t i = tid; i < live; i += SNT) {
+        uint32_t id = key_id(S.fin[i]);
+        S.fin[i] = make_key(exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim), id);
+      }
+      __syncthreads();
+      if (live <= 256) {
+        if (warp == 0) warp_sort_smem(S.fin, live, lane);
+      } else {
+        for (uint32_t j = live + tid; j < KP; j += SNT) S.fin[j] = kDummyKey;
+        __syncthreads();
+        block_sort_smem(S.fin, KP);
+      }
+      __syncthreads();
+    }
+    for (uint32_t i = tid; i < P.k; i += SNT) {
+      bool ok = i < live;
+      uint64_t e = ok ? S.fin[i] : kDummyKey;
+      P.out_ids[(size_t)qi * P.k + i] = ok ? key_id(e) : kInvalidId;
+      P.out_dists[(size_t)qi * P.k + i] = key_dist(e);
+    }
+    if (tid == 0) {
+      P.out_counts[qi] = live;
+      if (P.stats) {
+        DevStats st;
+        unsigned long long ev = 0;
+        uint32_t it = 0, cv = 1;
+        for (uint32_t t = 0; t < T; ++t) {
+          ev += ctl.evals[t];
+          it = max(it, ctl.iters[t]);
+          cv = cv && ctl.conv[t];
+        }
+        st.iterations = it;
+        st.hash_resets = 0;
+        st.distance_evals = ev;
+        st.converged = cv;
+        st.pad = 0;
+        P.stats[qi] = st;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) P.gens[blockIdx.x] = tag;
+}
+
+// ------------------------------------------------------------- dispatch ----
+uint32_t resolved_max_iter(uint32_t max_iter, uint32_t M, uint32_t p) {
+  if (max_iter) return max_iter;  // search.cpp:33-37
+  uint32_t it = (2 * M + p - 1) / p;
+  return it < 16 ? 16 : (it > 256 ? 256 : it);
+}
+
+// team / register-chunk variants: (team lanes, float4 chunks per lane)
+struct Variant {
+  int team, maxc;
+};
+
+Variant pick_variant(uint32_t ld, uint32_t req_team) {
+  uint32_t ch = ld / 4;
+  const Variant table[] = {{4, 2}, {8, 4}, {16, 4}, {32, 8}};
+  for (const Variant& v : table) {
+    if (req_team && (uint32_t)v.team != req_team) continue;
+    if ((uint32_t)(v.team * v.maxc) >= ch) return v;
+  }
+  return {32, 0};  // generic
+}
+
+using KernelFn = void (*)(const KParams);
+
+template <bool EXACT, bool SMEM>
+KernelFn per_query_fn(Variant v) {
+  if (EXACT) return search_kernel<32, 1, true, SMEM>;
+  switch (v.team * 100 + v.maxc) {
+    case 402: return search_kernel<4, 2, false, SMEM>;
+    case 804: return search_kernel<8, 4, false, SMEM>;
+    case 1604: return search_kernel<16, 4, false, SMEM>;
+    case 3208: return search_kernel<32, 8, false, SMEM>;
+    default: return search_kernel<32, 0, false, SMEM>;
+  }
+}
+
+KernelFn shared_fn(bool exact, Variant v) {
+  if (exact) return shared_search_kernel<32, 1, true>;
+  switch (v.team * 100 + v.maxc) {
+    case 402: return shared_search_kernel<4, 2, false>;
+    case 804: return shared_search_kernel<8, 4, false>;
+    case 1604: return shared_search_kernel<16, 4, false>;
+    case 3208: return shared_search_kernel<32, 8, false>;
+    default: return shared_search_kernel<32, 0, false>;
+  }
+}
+
+}  // namespace
+
+SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_t nq,
+                       int sm_count, size_t table_budget) {
+  SearchPlan pl;
+  const bool shared = c.mode == 1;
+  const uint32_t T = shared ? c.team_count : 1;
+  if (shared && (T < 2 || T > 16))
+    throw UsageErr("batch_search: shared mode supports 2 <= team_count <= 16 on device");
+  const uint32_t p = shared ? 1 : c.width;
+  const uint32_t d = ix.degree;
+  const uint32_t C = p * d;
+  const uint32_t imax = resolved_max_iter(c.max_iter, c.topm, p);
+  pl.teams = T;
+  pl.C = C;
+  pl.max_iter = imax;
+  pl.min_iter = shared ? std::min(c.min_iter, imax) : c.min_iter;  // engine.cpp:45
+  const bool forget = !shared && c.hash_policy == 1;
+  uint64_t hcap;
+  if (forget) {
+    hcap = 1ull << c.hash_bits;
+  } else {
+    // VisitedTable::standard_sized (search.cpp:104-108)
+    uint64_t expected = (uint64_t)(imax + 1) * (shared ? T : p) * d;
+    uint64_t want = 2 * std::max<uint64_t>(1, expected), cap = 1;
+    while (cap < want) cap <<= 1;
+    if (cap > (1ull << 31)) throw UsageErr("visited table capacity overflow");
+    hcap = cap;
+  }
+  pl.hcap = (uint32_t)hcap;
+  pl.smem_table = forget && hcap * 4 <= 32 * 1024;
+  const uint32_t ldr = round_up_u32(ix.ld, 4);
+  size_t smem;
+  if (!shared) {
+    uint32_t SP = next_pow2_u32(C);
+    smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * C + 2ull * round_up_u32(C, 2) +
+           4ull * round_up_u32(p, 4) + (pl.smem_table ? 4ull * hcap : 0);
+  } else {
+    if (d > 256) throw UsageErr("batch_search: shared mode on device needs graph degree <= 256");
+    uint32_t SP = next_pow2_u32(d), RP = next_pow2_u32(2 * T * d), KP = next_pow2_u32(c.k);
+    smem = 4ull * ldr + 16ull * c.topm * T + 8ull * SP * T + 8ull * KP + 8ull * RP +
+           8ull * T * d + 2ull * round_up_u32(T * d, 2) + 4ull * round_up_u32(T, 4);
+  }
+  if (smem > 200 * 1024)
+    throw UsageErr("search: parameters exceed the device shared-memory budget");
+  pl.smem = smem;
+  Variant v = pick_variant(ix.ld, c.team_size);
+  KernelFn fn = shared ? shared_fn(c.exact != 0, v)
+                       : (pl.smem_table ? (c.exact ? per_query_fn<true, true>(v)
+                                                   : per_query_fn<false, true>(v))
+                                        : (c.exact ? per_query_fn<true, false>(v)
+                                                   : per_query_fn<false, false>(v)));
+  pl.fn = reinterpret_cast<const void*>(fn);
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CAGRA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SNT, smem));
+  if (occ < 1) throw UsageErr("search: kernel cannot be resident with these parameters");
+  uint64_t grid = (uint64_t)sm_count * occ;
+  if (grid > nq) grid = nq ? nq : 1;
+  if (!pl.smem_table) {
+    uint64_t per = hcap * 8;
+    uint64_t maxg = table_budget / per;
+    if (maxg < 1) throw UsageErr("search: visited table exceeds the device memory budget");
+    if (grid > maxg) grid = maxg;
+    pl.table_elems = grid * hcap;
+  } else {
+    pl.table_elems = 0;
+  }
+  pl.grid = (uint32_t)grid;
+  pl.init_elems = (size_t)nq * T * C;
+  return pl;
+}
+
+uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const SearchPlan& pl,
+                       const float* d_queries, uint32_t nq, uint32_t* d_ids, float* d_dists,
+                       uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
+                       uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
+                       cudaStream_t stream) {
+  if (nq == 0) return 0;
+  dim3 ig((nq + 127) / 128, pl.teams);
+  init_samples_kernel<<<ig, 128, 0, stream>>>(nq, pl.teams > 1 ? ix.degree : pl.C, pl.teams,
+                                              ix.n, c.seed, c.seed_mode, c.query_offset,
+                                              d_init_ids);
+  CAGRA_LAUNCH_CHECK();
+  CAGRA_CUDA_TRY(cudaMemsetAsync(d_work, 0, sizeof(uint32_t), stream));
+  KParams P;
+  P.data = ix.data;
+  P.graph = ix.graph;
+  P.n = ix.n;
+  P.dim = ix.dim;
+  P.ld = ix.ld;
+  P.degree = ix.degree;
+  P.queries = d_queries;
+  P.nq = nq;
+  P.k = c.k;
+  P.M = c.topm;
+  P.p = pl.teams > 1 ? 1 : c.width;
+  P.C = pl.C;
+  P.max_iter = pl.max_iter;
+  P.min_iter = pl.min_iter;
+  P.policy = pl.teams > 1 ? 0 : c.hash_policy;
+  P.reset_interval = c.reset_interval ? c.reset_interval : 1;
+  P.hcap = pl.hcap;
+  P.teams = pl.teams;
+  P.init_ids = d_init_ids;
+  P.gtables = d_tables;
+  P.gens = d_gens;
+  P.work = d_work;
+  P.out_ids = d_ids;
+  P.out_dists = d_dists;
+  P.out_counts = d_counts;
+  P.stats = reinterpret_cast<DevStats*>(d_stats);
+  P.error = nullptr;
+  KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(pl.fn));
+  fn<<<pl.grid, SNT, pl.smem, stream>>>(P);
+  CAGRA_LAUNCH_CHECK();
+  return 2;
+}
+
+}  // namespace cagra
