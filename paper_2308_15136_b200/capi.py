@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcagra_b200.so")
+LIB_PATH = os.environ.get("CAGRA_LIB") or os.path.join(_HERE, "lib", "libcagra_b200.so")
 
 OK, ERR_USAGE, ERR_FORMAT, ERR_CUDA, ERR_NCCL, ERR_LOGIC = 0, 2, 3, 4, 5, 6
 HASH_STANDARD, HASH_FORGETTABLE = 0, 1

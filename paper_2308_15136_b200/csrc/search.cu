@@ -41,6 +41,11 @@ namespace cagra {
 namespace {
 
 constexpr int SNT = 256;  // threads per search CTA
+#ifdef CAGRA_DEBUG
+#define DBG(...) do { if (blockIdx.x == 0 && threadIdx.x == 0) printf(__VA_ARGS__); } while (0)
+#else
+#define DBG(...) do { } while (0)
+#endif
 constexpr int SWARPS = SNT / 32;
 
 struct DevStats {
@@ -284,7 +289,10 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
       qr[c] = ch < nchunk ? reinterpret_cast<const float4*>(S.q)[ch] : make_float4(0, 0, 0, 0);
     }
     constexpr int U = 2;  // rows in flight per team
-    for (uint32_t e0 = team; e0 < nev; e0 += NTEAMS * U) {
+    // warp-uniform trip count: every lane runs every iteration (the team
+    // shuffles below use the full mask)
+    for (uint32_t base = 0; base < nev; base += NTEAMS * U) {
+      const uint32_t e0 = base + team;
       float4 xv[U][MAXC];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -310,7 +318,7 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
           acc = fmaf(dw, dw, acc);
         }
 #pragma unroll
-        for (int o = TEAM / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int o = TEAM / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, TEAM);
         uint32_t e = e0 + u * NTEAMS;
         if (lt == 0 && e < nev) {
           uint32_t id = S.evlist[e];
@@ -644,13 +652,17 @@ search_kernel(const KParams P) {
     };
 
     // ---- init (search.cpp:192-201)
+    DBG("q%u init\n", qi);
     visit(init, false, P.C);
+    DBG("q%u init done nsurv=%u\n", qi, ctl.nsurv[0]);
     bool pending = true;
     uint32_t iters = 0;
     bool converged = false;
     for (;;) {
       // ---- step (search.cpp:218-245)
+      DBG("q%u it%u merge ns=%u\n", qi, iters, ctl.nsurv[0]);
       merge();
+      DBG("q%u it%u merged\n", qi, iters);
       pending = false;
       ++iters;
       // select_parents: first p unflagged non-dummy entries
@@ -681,6 +693,7 @@ search_kernel(const KParams P) {
         __syncthreads();
       }
       uint32_t np = ctl.npar[0];
+      DBG("q%u it%u np=%u\n", qi, iters, np);
       if (np == 0) {
         converged = iters >= P.min_iter;
         break;
@@ -696,7 +709,9 @@ search_kernel(const KParams P) {
       }
       if (iters >= P.max_iter) break;
     }
+    DBG("q%u loop done\n", qi);
     if (pending) merge();
+    DBG("q%u final merge\n", qi);
 
     // ---- finish (search.cpp:247-259)
     uint32_t live;
