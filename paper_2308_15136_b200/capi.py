@@ -81,7 +81,8 @@ class OptStatsC(C.Structure):
 EXPORTS = [
     "cagra_last_error", "cagra_version", "cagra_device_count", "cagra_search_params_default",
     "cagra_engine_opts_default", "cagra_uniform_dataset", "cagra_mix_seed",
-    "cagra_exact_knn_graph", "cagra_exact_topk", "cagra_count_detourable_routes",
+    "cagra_exact_knn_graph", "cagra_exact_topk", "cagra_knn_last_stats",
+    "cagra_count_detourable_routes",
     "cagra_reorder_and_prune", "cagra_build_reverse_graph", "cagra_merge_graphs",
     "cagra_optimize", "cagra_build_graph", "cagra_index_create", "cagra_index_create_dev",
     "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
@@ -108,6 +109,7 @@ def lib() -> C.CDLL:
         L.cagra_uniform_dataset.argtypes = [u64, u64, vp]
         L.cagra_exact_knn_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
         L.cagra_exact_topk.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp]
+        L.cagra_knn_last_stats.argtypes = [vp, vp, vp]
         L.cagra_count_detourable_routes.argtypes = [vp, vp, u32, u32, i32, vp]
         L.cagra_reorder_and_prune.argtypes = [vp, vp, u32, u32, u32, i32, vp]
         L.cagra_build_reverse_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
@@ -149,6 +151,14 @@ def device_count() -> int:
     c = C.c_int(0)
     lib().cagra_device_count(C.byref(c))
     return c.value
+
+
+def knn_last_stats() -> dict:
+    """Counters of the last tensor-core kNN / top-k call (rows, fallback_rows,
+    reranked); all zero when the SIMT path ran."""
+    v = (C.c_uint64 * 3)()
+    lib().cagra_knn_last_stats(C.byref(v, 0), C.byref(v, 8), C.byref(v, 16))
+    return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2]}
 
 
 def mix_seed(x: int) -> int:

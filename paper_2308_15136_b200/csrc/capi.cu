@@ -356,11 +356,11 @@ int cagra_exact_knn_graph(const float* data, uint32_t n, uint32_t dim, uint32_t 
     DeviceScope scope(dev);
     Stream st;
     uint32_t ld = row_stride(dim);
-    DBuf dd(sizeof(float) * (size_t)n * ld), sc(sizeof(uint64_t) * (size_t)n * k),
+    DBuf dd(sizeof(float) * (size_t)n * ld),
         di(sizeof(uint32_t) * (size_t)n * k), ds(sizeof(float) * (size_t)n * k);
     upload_rows(dd.as<float>(), data, n, dim, ld, st.s);
     launch_exact_topk(dd.as<float>(), n, ld, dd.as<float>(), n, ld, dim, k, true,
-                      sc.as<uint64_t>(), di.as<uint32_t>(), ds.as<float>(), st.s);
+                      di.as<uint32_t>(), ds.as<float>(), st.s);
     CAGRA_CUDA_TRY(cudaMemcpyAsync(ids_out, di.p, sizeof(uint32_t) * (size_t)n * k,
                                    cudaMemcpyDeviceToHost, st.s));
     CAGRA_CUDA_TRY(cudaMemcpyAsync(dists_out, ds.p, sizeof(float) * (size_t)n * k,
@@ -380,18 +380,25 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
     Stream st;
     uint32_t ld = row_stride(dim);
     DBuf dd(sizeof(float) * (size_t)n * ld), dq(sizeof(float) * (size_t)nq * ld),
-        sc(sizeof(uint64_t) * (size_t)nq * k), di(sizeof(uint32_t) * (size_t)nq * k),
+        di(sizeof(uint32_t) * (size_t)nq * k),
         ds(sizeof(float) * (size_t)nq * k);
     upload_rows(dd.as<float>(), data, n, dim, ld, st.s);
     upload_rows(dq.as<float>(), queries, nq, dim, ld, st.s);
     launch_exact_topk(dd.as<float>(), n, ld, dq.as<float>(), nq, ld, dim, k, false,
-                      sc.as<uint64_t>(), di.as<uint32_t>(), ds.as<float>(), st.s);
+                      di.as<uint32_t>(), ds.as<float>(), st.s);
     CAGRA_CUDA_TRY(cudaMemcpyAsync(ids_out, di.p, sizeof(uint32_t) * (size_t)nq * k,
                                    cudaMemcpyDeviceToHost, st.s));
     CAGRA_CUDA_TRY(cudaMemcpyAsync(dists_out, ds.p, sizeof(float) * (size_t)nq * k,
                                    cudaMemcpyDeviceToHost, st.s));
     st.sync();
   });
+}
+
+int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked) {
+  if (rows) *rows = g_knn_tc_stats.rows;
+  if (fallback_rows) *fallback_rows = g_knn_tc_stats.fallback_rows;
+  if (reranked) *reranked = g_knn_tc_stats.reranked;
+  return CAGRA_OK;
 }
 
 int cagra_count_detourable_routes(const uint32_t* knn_ids, const float* knn_dists, uint32_t n,
@@ -537,9 +544,8 @@ int cagra_build_graph(const float* data, uint32_t n, uint32_t dim, uint32_t d_in
     Event a, b;
     CAGRA_CUDA_TRY(cudaEventRecord(a.e, st.s));
     {
-      DBuf sc(sizeof(uint64_t) * e);
       launch_exact_topk(dd.as<float>(), n, ld, dd.as<float>(), n, ld, dim, d_init, true,
-                        sc.as<uint64_t>(), di.as<uint32_t>(), ds.as<float>(), st.s);
+                        di.as<uint32_t>(), ds.as<float>(), st.s);
       CAGRA_CUDA_TRY(cudaEventRecord(b.e, st.s));
       st.sync();
     }

@@ -81,6 +81,41 @@ __host__ __device__ __forceinline__ uint32_t round_up_u32(uint32_t x, uint32_t m
 }
 
 #ifdef __CUDACC__
+// Bitonic sort of 32*E keys held blocked in registers (index = lane*E + e).
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[E], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            int i = lane * E + e;
+            bool up = (i & k) == 0;
+            uint64_t a = v[e], b = v[e ^ j];
+            if ((a > b) == up) {
+              v[e] = b;
+              v[e ^ j] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          int i = lane * E + e;
+          uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+          bool up = (i & k) == 0;
+          bool lower = (i & j) == 0;
+          uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
 // The reference distance, dataset.hpp:33-43: strictly sequential fp32 chain,
 // separately rounded subtract, multiply and add (no FMA contraction).
 __device__ __forceinline__ float seq_step(float acc, float a, float b) {

@@ -9,14 +9,29 @@
 
 namespace cagra {
 
-// ---- knn_exact.cu -----------------------------------------------------------
+// ---- knn_exact.cu / knn_tc.cu -----------------------------------------------
 // Exact top-K by (dist, id) for nq query rows against n data rows (row
-// strides ld / qld floats).  exclude_self drops data index == query index
-// (the kNN graph, knn_build.cpp:52-60).  d_topk_scratch: nq*K u64.
+// strides ld / qld floats).  exclude_self drops data index == the query's own
+// index (the kNN graph, knn_build.cpp:52-60): self_ids[qi] when given, else qi.
+// Dispatcher: the tensor-core path (knn_tc.cu) when eligible, else SIMT.
 void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                        uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                       uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
-                       cudaStream_t stream);
+                       uint32_t* d_ids, float* d_dists, cudaStream_t stream);
+// SIMT register-tiled sequential-chain kernel.  d_topk_scratch: nq*K u64.
+void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
+                            uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K,
+                            bool exclude_self, const uint32_t* d_self_ids,
+                            uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
+                            cudaStream_t stream);
+// tcgen05 path (bf16x3 split GEMM + heap top-(K+32) + exact re-rank); synchronous.
+bool knn_tc_eligible(uint32_t dim, uint32_t K);
+void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
+                   uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
+                   uint32_t* d_ids, float* d_dists, cudaStream_t stream);
+struct KnnTcStats {
+  uint64_t rows = 0, fallback_rows = 0, reranked = 0;
+};
+extern KnnTcStats g_knn_tc_stats;
 
 // ---- graph_opt.cu -----------------------------------------------------------
 struct OptTimes {

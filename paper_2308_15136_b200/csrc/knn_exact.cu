@@ -94,7 +94,8 @@ __device__ void merge_row(int r, uint32_t K, uint64_t* __restrict__ row_topk, ui
 __global__ void __launch_bounds__(NT, 1)
 exact_topk_kernel(const float* __restrict__ data, uint32_t n, uint32_t ld,
                   const float* __restrict__ queries, uint32_t nq, uint32_t qld, uint32_t dim,
-                  uint32_t K, int exclude_self, uint64_t* __restrict__ topk,
+                  uint32_t K, int exclude_self, const uint32_t* __restrict__ self_ids,
+                  uint64_t* __restrict__ topk,
                   uint32_t* __restrict__ out_ids, float* __restrict__ out_dists) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw);            // BQ*CAP
@@ -167,7 +168,7 @@ exact_topk_kernel(const float* __restrict__ data, uint32_t n, uint32_t ld,
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint32_t j = t0 + tx + 16 * c;
-        if (j >= n || (exclude_self && j == qi)) continue;
+        if (j >= n || (exclude_self && j == (self_ids ? self_ids[qi] : qi))) continue;
         uint64_t key = make_key(acc[r][c], j);
         if (key < th) {
           uint32_t slot = atomicAdd(&cnt[row], 1u);
@@ -212,10 +213,11 @@ size_t exact_topk_smem(uint32_t K) {
 
 }  // namespace
 
-void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
-                       uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                       uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
-                       cudaStream_t stream) {
+void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
+                            uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K,
+                            bool exclude_self, const uint32_t* d_self_ids,
+                            uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
+                            cudaStream_t stream) {
   if (K > MAX_K) throw UsageErr("device exact top-k supports k <= 1024");
   if (nq == 0) return;
   size_t smem = exact_topk_smem(K);
@@ -223,9 +225,28 @@ void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((nq + BQ - 1) / BQ);
   exact_topk_kernel<<<grid, NT, smem, stream>>>(d_data, n, ld, d_queries, nq, qld, dim, K,
-                                                exclude_self ? 1 : 0, d_topk_scratch, d_ids,
-                                                d_dists);
+                                                exclude_self ? 1 : 0, d_self_ids, d_topk_scratch,
+                                                d_ids, d_dists);
   CAGRA_LAUNCH_CHECK();
+}
+
+void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
+                       uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
+                       uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
+  if (K > MAX_K) throw UsageErr("device exact top-k supports k <= 1024");
+  if (nq == 0) return;
+  if (knn_tc_eligible(dim, K)) {
+    launch_knn_tc(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, d_ids, d_dists,
+                  stream);
+    return;
+  }
+  g_knn_tc_stats = KnnTcStats{};
+  uint64_t* sc = nullptr;
+  CAGRA_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sc), sizeof(uint64_t) * nq * K,
+                                 stream));
+  launch_exact_topk_simt(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, nullptr, sc,
+                         d_ids, d_dists, stream);
+  CAGRA_CUDA_TRY(cudaFreeAsync(sc, stream));
 }
 
 }  // namespace cagra

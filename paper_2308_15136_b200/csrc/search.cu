@@ -93,41 +93,6 @@ __global__ void init_samples_kernel(uint32_t nq, uint32_t C, uint32_t teams, uin
 }
 
 // ------------------------------------------------------------ sorting ------
-// Bitonic sort of 32*E keys held blocked in registers (index = lane*E + e).
-template <int E>
-__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[E], int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32 * E; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < E) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if ((e & j) == 0) {
-            int i = lane * E + e;
-            bool up = (i & k) == 0;
-            uint64_t a = v[e], b = v[e ^ j];
-            if ((a > b) == up) {
-              v[e] = b;
-              v[e ^ j] = a;
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          int i = lane * E + e;
-          uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
-          bool up = (i & k) == 0;
-          bool lower = (i & j) == 0;
-          uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
-          v[e] = (lower == up) ? mn : mx;
-        }
-      }
-    }
-  }
-}
-
 template <int E>
 __device__ __forceinline__ void warp_sort_smem_E(uint64_t* a, uint32_t cnt, int lane) {
   uint64_t v[E];
