@@ -82,6 +82,33 @@ __host__ __device__ __forceinline__ uint32_t round_up_u32(uint32_t x, uint32_t m
 
 #ifdef __CUDACC__
 // Bitonic sort of 32*E keys held blocked in registers (index = lane*E + e).
+// Bitonic MERGE of a bitonic sequence of 32*E keys (ascending then
+// descending) held blocked in registers: log2(32E) compare-exchange stages.
+template <int E>
+__device__ __forceinline__ void warp_merge_regs(uint64_t (&v)[E], int lane) {
+#pragma unroll
+  for (int j = 16 * E; j > 0; j >>= 1) {
+    if (j < E) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if ((e & j) == 0) {
+          uint64_t a = v[e], b = v[e ^ j];
+          v[e] = a < b ? a : b;
+          v[e ^ j] = a < b ? b : a;
+        }
+      }
+    } else {
+      const bool lower = (lane & (j / E)) == 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+        uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+        v[e] = lower ? mn : mx;
+      }
+    }
+  }
+}
+
 template <int E>
 __device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[E], int lane) {
 #pragma unroll

@@ -3,20 +3,25 @@
 // (exact_topk, topk.cpp:10-43), bit-identical to the reference.
 //
 // 1. prep      : every fp32 row x is split into bf16 parts x = b0 + b1 + r
-//                (|r| <= 2^-16 |x|) and laid out as P = [b0 | b0 | b1] (query
-//                side) and R = [b0 | b1 | b0] (data side), K = 3*dim padded to
-//                64, so  P_q . R_x = b0.c0 + b0.c1 + b1.c0 ~= q . x  with
-//                relative error ~2^-16.  Squared norms and max |x| on the side.
+//                (|r| <= 2^-16 |x|), its squared norm n = n0 + n1 + n2 likewise,
+//                and laid out as
+//                  P_q = [-2b0 | -2b0 | -2b1 | 1 1 1 | n0 n1 n2 | 0..]  (query)
+//                  R_x = [  c0 |   c1 |   c0 | m0 m1 m2 | 1 1 1 | 0..]  (data)
+//                (K = 3*dim + 6 padded to 64), so the GEMM itself yields
+//                  P_q . R_x = |q|^2 + |x|^2 - 2 (b0.c0 + b0.c1 + b1.c0) = d~
+//                with relative error ~2^-16 on the cross term.
 // 2. knn_tc    : one CTA per 128 query rows.  The query tile (A) stays in smem
 //                for the whole sweep; 128-point data tiles (B) stream through
 //                a TMA ring (SWIZZLE_128B, K-major); one elected thread issues
 //                tcgen05.mma kind::f16 (bf16 x bf16 -> fp32) into a
 //                double-buffered TMEM accumulator (2 x 128 columns).  Four
-//                epilogue warps read the accumulator with tcgen05.ld (thread =
-//                query row = TMEM lane), form d~ = |q|^2 + |x|^2 - 2 q.x and
-//                keep each row's KC = k + 32 smallest (d~, id) keys in a
-//                per-row max-heap (L2-resident), fed through a shared-memory
-//                pending buffer so a warp drains its rows together.
+//                epilogue warps read d~ from the accumulator with tcgen05.ld
+//                (thread = query row = TMEM lane), build a 32-bit pass mask
+//                per 32 columns against the row's threshold (branch-free),
+//                append passing (d~, id) keys to a shared-memory pending
+//                buffer, and a warp merges full buffers into each row's sorted
+//                list of the KC = k + 32 smallest keys (L2-resident) with a
+//                warp-wide bitonic sort; the threshold is the list's last key.
 // 3. rerank    : per row (one warp), with delta = a rigorous bound on
 //                |d~ - d| for this row, every true top-k member has
 //                d~ <= d~_(k) + 2*delta; those candidates get the reference's
@@ -28,6 +33,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -44,6 +50,7 @@ constexpr int TC_BK = 64;     // bf16 per K-block (128 B rows, SWIZZLE_128B)
 constexpr int TC_STAGES = 4;  // B ring depth
 constexpr int TC_PEND = 64;   // pending keys per row in smem
 constexpr int TC_THREADS = 192;  // w0 TMA, w1 MMA, w2..w5 epilogue
+constexpr int TC_ACC = 4;        // TMEM accumulator ring (4 x 128 columns = all 512)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
 constexpr uint32_t TILE_BYTES = TC_BN * TC_BK * 2;  // 16 KB
 
@@ -128,33 +135,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                             ((uint32_t)(TC_BM >> 4) << 24);
 
-struct TcArgs {
-  uint32_t nq, n, kblocks, KC, exclude_self;
-  const float* qnorm;  // nq
-  const float* xnorm;  // n
-  uint64_t* heaps;     // nq * KC
-};
+__device__ unsigned long long g_tc_dbg[8];
 
-__device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t KC, uint64_t e) {
-  uint32_t i = 0;
-  for (;;) {
-    uint32_t l = 2 * i + 1;
-    if (l >= KC) break;
-    uint64_t big = h[l];
-    uint32_t bi = l;
-    if (l + 1 < KC) {
-      uint64_t r = h[l + 1];
-      if (r > big) {
-        big = r;
-        bi = l + 1;
-      }
-    }
-    if (big <= e) break;
-    h[i] = big;
-    i = bi;
-  }
-  h[i] = e;
-}
+struct TcArgs {
+  uint32_t nq, n, kblocks, KC, exclude_self, stages, dbg;
+  uint64_t* lists;  // nq * KC sorted keys (dist bits << 32 | id)
+};
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -163,33 +149,34 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   // 1024-byte alignment for the SWIZZLE_128B tiles
   unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
   unsigned char* sA = base;                                   // kblocks x 16 KB
-  unsigned char* sB = sA + (size_t)P.kblocks * TILE_BYTES;    // STAGES x 16 KB
-  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + TC_STAGES * TILE_BYTES);  // PEND x 128
+  unsigned char* sB = sA + (size_t)P.kblocks * TILE_BYTES;    // stages x 16 KB
+  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * TILE_BYTES);  // PEND x 128
   uint64_t* bars = pend + TC_PEND * TC_BM;
-  // bars: full[S] empty[S] afull tfull[2] tempty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 5);
+  // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * TC_ACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row0 = blockIdx.x * TC_BM;
   const uint32_t ntiles = (P.n + TC_BN - 1) / TC_BN;
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
-  const uint32_t afull = smem_u32(bars + 2 * TC_STAGES);
-  const uint32_t tfull0 = afull + 8, tempty0 = afull + 24;
+  const uint32_t S = P.stages;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
+  const uint32_t afull = smem_u32(bars + 2 * S);
+  const uint32_t tfull0 = afull + 8, tempty0 = afull + 8 + 8 * TC_ACC;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (uint32_t s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
     mbar_init(afull, 1);
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < TC_ACC; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -210,7 +197,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       uint32_t it = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
         for (uint32_t kb = 0; kb < P.kblocks; ++kb, ++it) {
-          const uint32_t s = it % TC_STAGES, ph = (it / TC_STAGES) & 1;
+          const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(empty0 + 8 * s, ph ^ 1);
           mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
           tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
@@ -225,12 +212,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tc_fence_after();
       uint32_t it = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
-        const uint32_t acc = t & 1, aph = (t >> 1) & 1;
+        const uint32_t acc = t % TC_ACC, aph = (t / TC_ACC) & 1;
         mbar_wait(tempty0 + 8 * acc, aph ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem + acc * TC_BN;
         for (uint32_t kb = 0; kb < P.kblocks; ++kb, ++it) {
-          const uint32_t s = it % TC_STAGES, ph = (it / TC_STAGES) & 1;
+          const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
           const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
@@ -249,27 +236,77 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t rl = q4 * 32 + lane;         // row within the tile
     const uint32_t row = row0 + rl;
     const bool live = row < P.nq;
-    uint64_t* heap = P.heaps + (size_t)(live ? row : 0) * P.KC;
-    if (live)
-      for (uint32_t i = 0; i < P.KC; ++i) heap[i] = kDummyKey;
-    const float qn = live ? P.qnorm[row] : 0.0f;
+    for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
+      const uint32_t rr = row0 + q4 * 32 + r;
+      if (rr < P.nq)
+        for (uint32_t i = lane; i < P.KC; i += 32) P.lists[(size_t)rr * P.KC + i] = kDummyKey;
+    }
+    __syncwarp();
     uint64_t tau = kDummyKey;
     float tau_f = __int_as_float(0x7f800000);
     uint32_t cnt = 0;
-    auto flush = [&]() {
-      for (uint32_t i = 0; i < cnt; ++i) {
-        uint64_t e = pend[i * TC_BM + rl];
-        if (e < tau) {
-          heap_replace_top(heap, P.KC, e);
-          tau = heap[0];
+    // Merge the pending keys of every lane with cnt > min_cnt into its row's
+    // sorted list, one row at a time, warp-wide: the pending keys are sorted
+    // (64 keys, 2 per lane) and appended in descending order behind the list
+    // (ascending, dummy padded to 192), and one bitonic merge of the 256 keys
+    // leaves the KC smallest in front.
+    auto flush = [&](uint32_t min_cnt) {
+      __syncwarp();
+      unsigned todo = __ballot_sync(0xffffffffu, cnt > min_cnt);
+      if (P.dbg == 3 && lane == 0) {
+        atomicAdd(&g_tc_dbg[0], 1ull);
+        atomicAdd(&g_tc_dbg[1], (unsigned long long)__popc(todo));
+      }
+      while (todo) {
+        const int r = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t rr = q4 * 32 + r;
+        const uint32_t rcnt = __shfl_sync(0xffffffffu, cnt, r);
+        uint64_t p[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t i = lane * 2 + e;
+          p[e] = i < rcnt ? pend[i * TC_BM + rr] : kDummyKey;
+        }
+        warp_sort_regs<2>(p, lane);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 2; ++e) pend[(lane * 2 + e) * TC_BM + rr] = p[e];
+        __syncwarp();
+        uint64_t* lst = P.lists + (size_t)(row0 + rr) * P.KC;
+        uint64_t v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t i = lane * 8 + e;
+          v[e] = i < P.KC ? lst[i] : (i < 192 ? kDummyKey : pend[(255 - i) * TC_BM + rr]);
+        }
+        warp_merge_regs<8>(v, lane);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t i = lane * 8 + e;
+          if (i < P.KC) lst[i] = v[e];
+        }
+        // new threshold: key KC-1 (lane (KC-1)/8, slot (KC-1)%8)
+        const uint32_t last = P.KC - 1;
+        uint64_t lastv = v[0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e)
+          if ((uint32_t)e == last % 8) lastv = v[e];
+        lastv = __shfl_sync(0xffffffffu, lastv, last / 8);
+        if (lane == r) {
+          tau = lastv;
+          tau_f = key_dist(tau);
+          cnt = 0;
         }
       }
-      cnt = 0;
-      tau_f = key_dist(tau);
+      __syncwarp();
     };
+    long long t_start = clock64(), t_wait = 0;
     for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t acc = t & 1, aph = (t >> 1) & 1;
+      const uint32_t acc = t % TC_ACC, aph = (t / TC_ACC) & 1;
+      long long tw = clock64();
       mbar_wait(tfull0 + 8 * acc, aph);
+      t_wait += clock64() - tw;
       tc_fence_after();
       for (uint32_t c = 0; c < TC_BN / 32; ++c) {
         uint32_t v[32];
@@ -278,33 +315,76 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           tc_fence_before();
           mbar_arrive(tempty0 + 8 * acc);
         }
-        const uint32_t cbase = t * TC_BN + c * 32;
-        const float xn_l = cbase + lane < P.n ? __ldg(P.xnorm + cbase + lane) : 0.0f;
+        if (P.dbg == 1) continue;
+        // fast path: the chunk's minimum against the threshold (FMNMX3 tree)
+        float m3[11];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float xn = __shfl_sync(0xffffffffu, xn_l, i);
-          float d = fmaf(-2.0f, __uint_as_float(v[i]), qn + xn);
-          d = fmaxf(d, 0.0f);
-          const uint32_t col = cbase + i;
-          if (d <= tau_f && live && col < P.n && !(P.exclude_self && col == row)) {
-            pend[cnt * TC_BM + rl] = make_key(d, col);
-            ++cnt;
+        for (int i = 0; i < 10; ++i) {
+          float r3;
+          asm("min.f32 %0, %1, %2, %3;"
+              : "=f"(r3)
+              : "f"(__uint_as_float(v[3 * i])), "f"(__uint_as_float(v[3 * i + 1])),
+                "f"(__uint_as_float(v[3 * i + 2])));
+          m3[i] = r3;
+        }
+        m3[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+        float mn;
+        {
+          float a0, a1, a2, a3;
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(a0) : "f"(m3[0]), "f"(m3[1]), "f"(m3[2]));
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(a1) : "f"(m3[3]), "f"(m3[4]), "f"(m3[5]));
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(a2) : "f"(m3[6]), "f"(m3[7]), "f"(m3[8]));
+          a3 = fminf(m3[9], m3[10]);
+          float b0;
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(b0) : "f"(a0), "f"(a1), "f"(a2));
+          mn = fminf(b0, a3);
+        }
+        const bool hit = live && mn <= tau_f;
+        if (P.dbg == 2) {
+          if (hit && mn == 12345.0f) cnt++;
+          continue;
+        }
+        if (__any_sync(0xffffffffu, hit)) {
+          if (P.dbg == 3 && lane == 0) atomicAdd(&g_tc_dbg[3], 1ull);
+          const uint32_t cbase = t * TC_BN + c * 32;
+          uint32_t m = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) m |= (__uint_as_float(v[i]) <= tau_f ? 1u : 0u) << i;
+          if (cbase + 32 > P.n) m &= cbase >= P.n ? 0u : (1u << (P.n - cbase)) - 1u;
+          if (P.exclude_self && row - cbase < 32u) m &= ~(1u << (row - cbase));
+          if (!hit) m = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if ((m >> i) & 1u) {
+              pend[cnt * TC_BM + rl] = make_key(fmaxf(__uint_as_float(v[i]), 0.0f), cbase + i);
+              ++cnt;
+            }
+          }
+          if (__any_sync(0xffffffffu, cnt > TC_PEND - 32)) {
+            long long t0 = clock64();
+            flush(TC_PEND / 4);
+            if (P.dbg == 3 && lane == 0) atomicAdd(&g_tc_dbg[4], (unsigned long long)(clock64() - t0));
           }
         }
-        if (__any_sync(0xffffffffu, cnt > TC_PEND - 32)) flush();
       }
     }
-    flush();
+    flush(0);
+    if (P.dbg == 3 && lane == 0) {
+      atomicAdd(&g_tc_dbg[5], (unsigned long long)(clock64() - t_start));
+      atomicAdd(&g_tc_dbg[6], (unsigned long long)t_wait);
+    }
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
 // ----------------------------------------------------------------- prep ----
-// x = b0 + b1 + r;  P = [b0 | b0 | b1 | 0],  R = [b0 | b1 | b0 | 0]
+// x = b0 + b1 + r,  |x|^2 = n0 + n1 + n2 (bf16 parts)
+//   query side P = [-2b0 | -2b0 | -2b1 | 1 1 1 | n0 n1 n2 | 0]
+//   data side  R = [  b0 |   b1 |   b0 | n0 n1 n2 | 1 1 1 | 0]
 __global__ void tc_split_kernel(const float* __restrict__ src, uint32_t rows, uint32_t ld,
                                 uint32_t dim, uint32_t Kp, __nv_bfloat16* __restrict__ P,
                                 __nv_bfloat16* __restrict__ R, float* __restrict__ norms,
@@ -315,30 +395,37 @@ __global__ void tc_split_kernel(const float* __restrict__ src, uint32_t rows, ui
   const float* x = src + (size_t)row * ld;
   __nv_bfloat16* p = P ? P + (size_t)row * Kp : nullptr;
   __nv_bfloat16* r = R ? R + (size_t)row * Kp : nullptr;
+  const __nv_bfloat16 zero = __float2bfloat16_rn(0.0f), one = __float2bfloat16_rn(1.0f);
   float ss = 0.0f;
-  for (uint32_t i = lane; i < Kp; i += 32) {
-    if (i < dim) {
-      float v = x[i];
-      ss = fmaf(v, v, ss);
-      __nv_bfloat16 b0 = __float2bfloat16_rn(v);
-      __nv_bfloat16 b1 = __float2bfloat16_rn(v - __bfloat162float(b0));
-      if (p) {
-        p[i] = b0;
-        p[dim + i] = b0;
-        p[2 * dim + i] = b1;
-      }
-      if (r) {
-        r[i] = b0;
-        r[dim + i] = b1;
-        r[2 * dim + i] = b0;
-      }
-    } else if (i >= 3 * dim) {
-      if (p) p[i] = __float2bfloat16_rn(0.0f);
-      if (r) r[i] = __float2bfloat16_rn(0.0f);
+  for (uint32_t i = lane; i < dim; i += 32) {
+    float v = x[i];
+    ss = fmaf(v, v, ss);
+    __nv_bfloat16 b0 = __float2bfloat16_rn(v);
+    __nv_bfloat16 b1 = __float2bfloat16_rn(v - __bfloat162float(b0));
+    if (p) {
+      __nv_bfloat16 m0 = __float2bfloat16_rn(-2.0f * __bfloat162float(b0));  // exact
+      __nv_bfloat16 m1 = __float2bfloat16_rn(-2.0f * __bfloat162float(b1));
+      p[i] = m0;
+      p[dim + i] = m0;
+      p[2 * dim + i] = m1;
+    }
+    if (r) {
+      r[i] = b0;
+      r[dim + i] = b1;
+      r[2 * dim + i] = b0;
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const __nv_bfloat16 n0 = __float2bfloat16_rn(ss);
+  const float rem = ss - __bfloat162float(n0);
+  const __nv_bfloat16 n1 = __float2bfloat16_rn(rem);
+  const __nv_bfloat16 n2 = __float2bfloat16_rn(rem - __bfloat162float(n1));
+  for (uint32_t i = 3 * dim + lane; i < Kp; i += 32) {
+    const uint32_t j = i - 3 * dim;
+    if (p) p[i] = j < 3 ? one : (j == 3 ? n0 : (j == 4 ? n1 : (j == 5 ? n2 : zero)));
+    if (r) r[i] = j == 0 ? n0 : (j == 1 ? n1 : (j == 2 ? n2 : (j < 6 ? one : zero)));
+  }
   if (lane == 0) {
     norms[row] = ss;
     if (maxnorm_bits) atomicMax(maxnorm_bits, __float_as_uint(ss));
@@ -349,7 +436,7 @@ __global__ void tc_split_kernel(const float* __restrict__ src, uint32_t rows, ui
 // One warp per query row: band selection on d~, exact sequential-chain
 // distances, (dist, id) sort, first k.  Rows whose band overflows the KC keys
 // are queued for the exact SIMT kernel.
-__global__ void tc_rerank_kernel(const uint64_t* __restrict__ heaps, uint32_t nq, uint32_t KC,
+__global__ void tc_rerank_kernel(const uint64_t* __restrict__ lists, uint32_t nq, uint32_t KC,
                                  uint32_t K, const float* __restrict__ qnorm,
                                  const uint32_t* __restrict__ maxnorm_bits, float eps_rel,
                                  float eps_norm, const float* __restrict__ data, uint32_t ld,
@@ -365,7 +452,7 @@ __global__ void tc_rerank_kernel(const uint64_t* __restrict__ heaps, uint32_t nq
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     uint32_t i = lane * E + e;
-    v[e] = i < KC ? heaps[(size_t)row * KC + i] : kDummyKey;
+    v[e] = i < KC ? lists[(size_t)row * KC + i] : kDummyKey;
   }
   warp_sort_regs<E>(v, lane);
   // number of real keys (dummies sort last)
@@ -481,9 +568,17 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp) {
   return tm;
 }
 
-size_t tc_smem_bytes(uint32_t kblocks) {
-  return 1024 + (size_t)kblocks * TILE_BYTES + TC_STAGES * TILE_BYTES +
-         sizeof(uint64_t) * (TC_PEND * TC_BM + 2 * TC_STAGES + 5) + 16;
+size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages) {
+  return 1024 + (size_t)kblocks * TILE_BYTES + stages * TILE_BYTES +
+         sizeof(uint64_t) * (TC_PEND * TC_BM + 2 * stages + 1 + 2 * TC_ACC) + 16;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+uint32_t tc_stages(uint32_t kblocks) {
+  uint32_t s = TC_STAGES;
+  while (s > 2 && tc_smem_bytes(kblocks, s) > kSmemLimit) --s;
+  return s;
 }
 
 }  // namespace
@@ -493,19 +588,20 @@ KnnTcStats g_knn_tc_stats;
 bool knn_tc_eligible(uint32_t dim, uint32_t K) {
   const char* env = std::getenv("CAGRA_KNN_PATH");
   if (env && std::strcmp(env, "simt") == 0) return false;
-  uint32_t Kp = round_up_u32(3 * dim, TC_BK);
-  return Kp / TC_BK <= TC_MAX_KB && K + 32 <= 256;
+  uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK);
+  return Kp / TC_BK <= TC_MAX_KB && tc_smem_bytes(Kp / TC_BK, tc_stages(Kp / TC_BK)) <= kSmemLimit &&
+         K + 32 + TC_PEND <= 256;
 }
 
 void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
                    uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
   if (nq == 0) return;
-  const uint32_t Kp = round_up_u32(3 * dim, TC_BK), kblocks = Kp / TC_BK;
-  const uint32_t KC = K + 32;  // heap size (dummy keys pad inputs with fewer points)
+  const uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK), kblocks = Kp / TC_BK;
+  const uint32_t KC = K + 32;  // list size (dummy keys pad inputs with fewer points)
   const bool same = exclude_self;  // kNN graph: queries are the data rows
   Dev dP((size_t)nq * Kp * 2), dR((size_t)n * Kp * 2), dqn(4ull * nq),
-      dxn(4ull * n), dmax(4), heaps(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
+      dxn(4ull * n), dmax(4), lists(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
   CAGRA_CUDA_TRY(cudaMemsetAsync(dmax.p, 0, 4, stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
@@ -530,25 +626,38 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   a.kblocks = kblocks;
   a.KC = KC;
   a.exclude_self = exclude_self ? 1 : 0;
-  a.qnorm = qnorm;
-  a.xnorm = dxn.as<float>();
-  a.heaps = heaps.as<uint64_t>();
-  size_t smem = tc_smem_bytes(kblocks);
+  a.lists = lists.as<uint64_t>();
+  a.stages = tc_stages(kblocks);
+  const char* dbg = std::getenv("CAGRA_TC_DEBUG");
+  a.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
+  size_t smem = tc_smem_bytes(kblocks, a.stages);
   CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, stream>>>(tmA, tmB, a);
   CAGRA_LAUNCH_CHECK();
-  // error bound of d~ (see file header): split ~3.1*2^-16, fp32 accumulation
-  // over Kp terms, norms over dim terms; x2 for the -2 q.x term.
-  const float eps_rel = 2.0f * (3.1f * 1.52587890625e-05f + (float)Kp * 1.1920929e-07f);
-  const float eps_norm = (float)(dim + 8) * 2.384185791e-07f;
+  // error bound of d~ (file header): |d~ - d| <= eps_rel |q| max|x| +
+  // eps_norm (|q|^2 + max|x|^2): the split's omitted terms (3.1*2^-16 of
+  // sum|q_i||x_i| <= |q||x|, doubled by the -2), fp32 accumulation over Kp
+  // terms of total magnitude 2|q||x| + |q|^2 + |x|^2, and the fp32 norms.
+  const float u23 = 1.1920929e-07f;
+  const float eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)Kp * u23;
+  const float eps_norm = (float)Kp * u23 + (float)(dim + 8) * u23;
   uint32_t* fail_rows = fails.as<uint32_t>() + 1;
   uint32_t* fail_cnt = fails.as<uint32_t>();
   tc_rerank_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
-      heaps.as<uint64_t>(), nq, KC, K, qnorm, dmax.as<uint32_t>(), eps_rel, eps_norm, d_data, ld,
+      lists.as<uint64_t>(), nq, KC, K, qnorm, dmax.as<uint32_t>(), eps_rel, eps_norm, d_data, ld,
       d_queries, qld, dim, d_ids, d_dists, fail_rows, fail_cnt,
       rer.as<unsigned long long>());
   CAGRA_LAUNCH_CHECK();
+  if (a.dbg == 3) {
+    unsigned long long h[8];
+    CAGRA_CUDA_TRY(cudaMemcpyFromSymbol(h, g_tc_dbg, sizeof(h)));
+    fprintf(stderr, "tc dbg: flush events %llu row-flushes %llu keys flushed %llu slow chunks %llu"
+                    " (warps %u) cycles: flush %llu total %llu wait-tfull %llu\n", h[0], h[1], h[2],
+            h[3], (nq + 127) / 128 * 4, h[4], h[5], h[6]);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CAGRA_CUDA_TRY(cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)));
+  }
   uint32_t nf = 0;
   unsigned long long nre = 0;
   CAGRA_CUDA_TRY(cudaMemcpyAsync(&nf, fail_cnt, 4, cudaMemcpyDeviceToHost, stream));
