@@ -134,11 +134,13 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
                      uint32_t nq, uint32_t k, int device, uint32_t* ids_out,
                      float* dists_out);
 
-/* Counters of the last tensor-core kNN / top-k call on this thread's process:
- * rows processed, rows re-done by the exact SIMT kernel because their
- * candidate band overflowed, candidates re-ranked with the sequential chain.
- * Any pointer may be NULL. */
-int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked);
+/* Counters of the last tensor-core kNN / top-k call in this process: rows
+ * processed, rows re-done by the exact SIMT kernel because their candidate
+ * band overflowed, candidates re-ranked with the sequential chain, rows whose
+ * sample-pass threshold did not bracket their band (re-done by the
+ * single-pass list mode).  Any pointer may be NULL. */
+int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked,
+                         uint64_t* retried_rows);
 
 /* ---- graph optimization (rank mode) -------------------------------------- */
 /* count_detourable_routes (graph_opt.hpp:47-49), rank mode.  Rejects rows not

@@ -109,7 +109,7 @@ def lib() -> C.CDLL:
         L.cagra_uniform_dataset.argtypes = [u64, u64, vp]
         L.cagra_exact_knn_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
         L.cagra_exact_topk.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp]
-        L.cagra_knn_last_stats.argtypes = [vp, vp, vp]
+        L.cagra_knn_last_stats.argtypes = [vp, vp, vp, vp]
         L.cagra_count_detourable_routes.argtypes = [vp, vp, u32, u32, i32, vp]
         L.cagra_reorder_and_prune.argtypes = [vp, vp, u32, u32, u32, i32, vp]
         L.cagra_build_reverse_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
@@ -156,9 +156,9 @@ def device_count() -> int:
 def knn_last_stats() -> dict:
     """Counters of the last tensor-core kNN / top-k call (rows, fallback_rows,
     reranked); all zero when the SIMT path ran."""
-    v = (C.c_uint64 * 3)()
-    lib().cagra_knn_last_stats(C.byref(v, 0), C.byref(v, 8), C.byref(v, 16))
-    return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2]}
+    v = (C.c_uint64 * 4)()
+    lib().cagra_knn_last_stats(C.byref(v, 0), C.byref(v, 8), C.byref(v, 16), C.byref(v, 24))
+    return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2], "retried_rows": v[3]}
 
 
 def mix_seed(x: int) -> int:

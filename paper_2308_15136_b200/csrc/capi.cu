@@ -394,7 +394,9 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
   });
 }
 
-int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked) {
+int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked,
+                         uint64_t* retried_rows) {
+  if (retried_rows) *retried_rows = g_knn_tc_stats.retried_rows;
   if (rows) *rows = g_knn_tc_stats.rows;
   if (fallback_rows) *fallback_rows = g_knn_tc_stats.fallback_rows;
   if (reranked) *reranked = g_knn_tc_stats.reranked;

@@ -29,7 +29,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
                    uint32_t* d_ids, float* d_dists, cudaStream_t stream);
 struct KnnTcStats {
-  uint64_t rows = 0, fallback_rows = 0, reranked = 0;
+  uint64_t rows = 0, fallback_rows = 0, reranked = 0, retried_rows = 0;
 };
 extern KnnTcStats g_knn_tc_stats;
 

@@ -22,6 +22,12 @@
 //                buffer, and a warp merges full buffers into each row's sorted
 //                list of the KC = k + 32 smallest keys (L2-resident) with a
 //                warp-wide bitonic sort; the threshold is the list's last key.
+//                Two passes when N >= 64k: pass 1 runs this over every 16th
+//                point keeping the r smallest (r ~ 3(k+16)/16); the r-th
+//                smallest d~ of any subset is an upper bound tau* of the r-th
+//                smallest overall, so pass 2 over all points just appends
+//                every d~ <= tau* (~3(k+16) per row) — no merging.  Rows
+//                whose tau* does not bracket their band re-run single-pass.
 // 3. rerank    : per row (one warp), with delta = a rigorous bound on
 //                |d~ - d| for this row, every true top-k member has
 //                d~ <= d~_(k) + 2*delta; those candidates get the reference's
@@ -48,7 +54,7 @@ constexpr int TC_BM = 128;    // query rows per CTA (= TMEM lanes)
 constexpr int TC_BN = 128;    // data points per tile (= accumulator columns)
 constexpr int TC_BK = 64;     // bf16 per K-block (128 B rows, SWIZZLE_128B)
 constexpr int TC_STAGES = 4;  // B ring depth
-constexpr int TC_PEND = 64;   // pending keys per row in smem
+constexpr int TC_PEND = 48;   // pending keys per row in smem
 constexpr int TC_THREADS = 192;  // w0 TMA, w1 MMA, w2..w5 epilogue
 constexpr int TC_ACC = 4;        // TMEM accumulator ring (4 x 128 columns = all 512)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
@@ -109,8 +115,8 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
       : "memory");
 }
-// 32 lanes x 32 consecutive columns -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+// 32 lanes x 32 consecutive columns -> 32 registers per thread (no wait).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -122,9 +128,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
         "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of
 // 1024 B (SBO), sm_100 descriptor version 1.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -139,7 +143,15 @@ __device__ unsigned long long g_tc_dbg[8];
 
 struct TcArgs {
   uint32_t nq, n, kblocks, KC, exclude_self, stages, dbg;
-  uint64_t* lists;  // nq * KC sorted keys (dist bits << 32 | id)
+  uint32_t mode;        // 0: running sorted list of KC keys; 1: append d~ <= fixed tau
+  uint32_t col_stride;  // B row c is data point c * col_stride (sample pass)
+  uint64_t* lists;      // mode 0: nq * KC sorted keys (dist bits << 32 | id)
+  const uint64_t* tau_keys;  // mode 1: row's threshold = key_dist(tau_keys[row * tau_ld + tau_ld - 1])
+  uint32_t tau_ld;
+  uint64_t* bufs;       // mode 1: nq * capg appended keys
+  uint32_t* bcount;     // mode 1: keys appended per row (capg + 1 = overflow)
+  uint32_t capg;
+  const uint32_t* self_ids;  // optional: data id of each query row (self exclusion)
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -151,7 +163,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   unsigned char* sA = base;                                   // kblocks x 16 KB
   unsigned char* sB = sA + (size_t)P.kblocks * TILE_BYTES;    // stages x 16 KB
   uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * TILE_BYTES);  // PEND x 128
-  uint64_t* bars = pend + TC_PEND * TC_BM;
+  float* scratch = reinterpret_cast<float*>(pend + TC_PEND * TC_BM);  // 128 rows x 33
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + TC_BM * 33 + 8);
   // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * TC_ACC);
 
@@ -236,15 +249,38 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t rl = q4 * 32 + lane;         // row within the tile
     const uint32_t row = row0 + rl;
     const bool live = row < P.nq;
-    for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
-      const uint32_t rr = row0 + q4 * 32 + r;
-      if (rr < P.nq)
-        for (uint32_t i = lane; i < P.KC; i += 32) P.lists[(size_t)rr * P.KC + i] = kDummyKey;
+    if (P.mode == 0) {
+      for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
+        const uint32_t rr = row0 + q4 * 32 + r;
+        if (rr < P.nq)
+          for (uint32_t i = lane; i < P.KC; i += 32) P.lists[(size_t)rr * P.KC + i] = kDummyKey;
+      }
     }
     __syncwarp();
     uint64_t tau = kDummyKey;
     float tau_f = __int_as_float(0x7f800000);
-    uint32_t cnt = 0;
+    if (P.mode == 1 && live)
+      tau_f = key_dist(P.tau_keys[(size_t)row * P.tau_ld + P.tau_ld - 1]);
+    uint32_t cnt = 0, gcnt = 0;
+    // this row's own column in B coordinates (self exclusion), or none
+    const uint32_t self_id = live && P.self_ids ? P.self_ids[row] : row;
+    const uint32_t self_c = (P.exclude_self && self_id % P.col_stride == 0)
+                                ? self_id / P.col_stride
+                                : 0xffffffffu;
+    // append mode: copy every lane's pending keys to its row's global buffer
+    auto spill = [&]() {
+      if (live && cnt) {
+        if (gcnt + cnt <= P.capg) {
+          uint64_t* b = P.bufs + (size_t)row * P.capg + gcnt;
+          for (uint32_t i = 0; i < cnt; ++i) b[i] = pend[i * TC_BM + rl];
+          gcnt += cnt;
+        } else {
+          gcnt = P.capg + 1;  // overflow: the row is redone by the fallback
+        }
+      }
+      cnt = 0;
+      __syncwarp();
+    };
     // Merge the pending keys of every lane with cnt > min_cnt into its row's
     // sorted list, one row at a time, warp-wide: the pending keys are sorted
     // (64 keys, 2 per lane) and appended in descending order behind the list
@@ -271,14 +307,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         warp_sort_regs<2>(p, lane);
         __syncwarp();
 #pragma unroll
-        for (int e = 0; e < 2; ++e) pend[(lane * 2 + e) * TC_BM + rr] = p[e];
+        for (int e = 0; e < 2; ++e)
+          if (lane * 2 + e < TC_PEND) pend[(lane * 2 + e) * TC_BM + rr] = p[e];
         __syncwarp();
         uint64_t* lst = P.lists + (size_t)(row0 + rr) * P.KC;
         uint64_t v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const uint32_t i = lane * 8 + e;
-          v[e] = i < P.KC ? lst[i] : (i < 192 ? kDummyKey : pend[(255 - i) * TC_BM + rr]);
+          v[e] = i < P.KC ? lst[i]
+                          : (i < 256 - TC_PEND ? kDummyKey : pend[(255 - i) * TC_BM + rr]);
         }
         warp_merge_regs<8>(v, lane);
 #pragma unroll
@@ -308,9 +346,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       mbar_wait(tfull0 + 8 * acc, aph);
       t_wait += clock64() - tw;
       tc_fence_after();
+#pragma unroll 1
       for (uint32_t c = 0; c < TC_BN / 32; ++c) {
         uint32_t v[32];
-        tmem_ld32(tmem + ((q4 * 32) << 16) + acc * TC_BN + c * 32, v);
+        tmem_ld32_nowait(tmem + ((q4 * 32) << 16) + acc * TC_BN + c * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == TC_BN / 32 - 1) {
           tc_fence_before();
           mbar_arrive(tempty0 + 8 * acc);
@@ -339,36 +379,38 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           asm("min.f32 %0, %1, %2, %3;" : "=f"(b0) : "f"(a0), "f"(a1), "f"(a2));
           mn = fminf(b0, a3);
         }
-        const bool hit = live && mn <= tau_f;
-        if (P.dbg == 2) {
-          if (hit && mn == 12345.0f) cnt++;
-          continue;
-        }
-        if (__any_sync(0xffffffffu, hit)) {
-          if (P.dbg == 3 && lane == 0) atomicAdd(&g_tc_dbg[3], 1ull);
-          const uint32_t cbase = t * TC_BN + c * 32;
-          uint32_t m = 0;
+        const bool hit = live && mn <= tau_f && gcnt <= P.capg;
+        if (!__any_sync(0xffffffffu, hit)) continue;
+        // slow path: stash the chunk, then walk the passing bits
+        const uint32_t cbase = t * TC_BN + c * 32;
+        uint32_t m = 0;
+        if (hit) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) m |= (__uint_as_float(v[i]) <= tau_f ? 1u : 0u) << i;
           if (cbase + 32 > P.n) m &= cbase >= P.n ? 0u : (1u << (P.n - cbase)) - 1u;
-          if (P.exclude_self && row - cbase < 32u) m &= ~(1u << (row - cbase));
-          if (!hit) m = 0;
+          if (self_c - cbase < 32u) m &= ~(1u << (self_c - cbase));
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if ((m >> i) & 1u) {
-              pend[cnt * TC_BM + rl] = make_key(fmaxf(__uint_as_float(v[i]), 0.0f), cbase + i);
-              ++cnt;
-            }
-          }
-          if (__any_sync(0xffffffffu, cnt > TC_PEND - 32)) {
-            long long t0 = clock64();
-            flush(TC_PEND / 4);
-            if (P.dbg == 3 && lane == 0) atomicAdd(&g_tc_dbg[4], (unsigned long long)(clock64() - t0));
-          }
+          for (int i = 0; i < 32; ++i) scratch[rl * 33 + i] = __uint_as_float(v[i]);
+        }
+        while (m) {
+          const int i = __ffs(m) - 1;
+          m &= m - 1;
+          pend[cnt * TC_BM + rl] =
+              make_key(fmaxf(scratch[rl * 33 + i], 0.0f), (cbase + i) * P.col_stride);
+          ++cnt;
+        }
+        if (__any_sync(0xffffffffu, cnt > TC_PEND - 32)) {
+          if (P.mode == 0) flush(TC_PEND / 4);
+          else spill();
         }
       }
     }
-    flush(0);
+    if (P.mode == 0) {
+      flush(0);
+    } else {
+      spill();
+      if (live) P.bcount[row] = gcnt;
+    }
     if (P.dbg == 3 && lane == 0) {
       atomicAdd(&g_tc_dbg[5], (unsigned long long)(clock64() - t_start));
       atomicAdd(&g_tc_dbg[6], (unsigned long long)t_wait);
@@ -501,6 +543,112 @@ __global__ void tc_rerank_kernel(const uint64_t* __restrict__ lists, uint32_t nq
   if (lane == 0 && reranked) atomicAdd(reranked, (unsigned long long)nre);
 }
 
+// Append-mode rerank: one warp per row.  The buffer holds EVERY point with
+// d~ <= tau* (tau* from the sample pass).  Valid iff K <= count <= capg and
+// d~_(K) + 2 delta <= tau* (then every point that can be a true top-K member
+// is in the buffer); otherwise the row is queued for the list-mode pass.
+__global__ void tc_rerank_append_kernel(uint64_t* __restrict__ bufs,
+                                        const uint32_t* __restrict__ bcount, uint32_t capg,
+                                        const uint64_t* __restrict__ tau_keys, uint32_t tau_ld,
+                                        uint32_t nq, uint32_t K, const float* __restrict__ qnorm,
+                                        const uint32_t* __restrict__ maxnorm_bits, float eps_rel,
+                                        float eps_norm, const float* __restrict__ data, uint32_t ld,
+                                        const float* __restrict__ queries, uint32_t qld,
+                                        uint32_t dim, uint32_t* __restrict__ out_ids,
+                                        float* __restrict__ out_dists,
+                                        uint32_t* __restrict__ fail_rows,
+                                        uint32_t* __restrict__ fail_cnt,
+                                        unsigned long long* __restrict__ reranked) {
+  const uint32_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= nq) return;
+  const uint32_t c = bcount[row];
+  const float tau_star = key_dist(tau_keys[(size_t)row * tau_ld + tau_ld - 1]);
+  uint64_t* b = bufs + (size_t)row * capg;
+  bool ok = c >= K && c <= capg;
+  float bound = 0.0f;
+  if (ok) {
+    constexpr int E = 32;  // up to 1024 keys
+    uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = lane * E + e;
+      v[e] = i < c ? b[i] : kDummyKey;
+    }
+    warp_sort_regs<E>(v, lane);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = lane * E + e;
+      if (i < c) b[i] = v[e];
+    }
+    __syncwarp();
+    const float qn = qnorm[row];
+    const float xm = __uint_as_float(*maxnorm_bits);
+    const float delta = eps_rel * sqrtf(qn) * sqrtf(xm) + eps_norm * (qn + xm);
+    bound = key_dist(b[K - 1]) + 2.0f * delta;
+    ok = bound <= tau_star;
+  }
+  if (!ok) {
+    if (lane == 0) fail_rows[atomicAdd(fail_cnt, 1u)] = row;
+    return;
+  }
+  // exact sequential-chain distances for the band, cyclic over lanes
+  constexpr int E2 = 8;
+  uint64_t w[E2];
+  const float* q = queries + (size_t)row * qld;
+  uint32_t nre = 0;
+  bool over = false;
+#pragma unroll
+  for (int e = 0; e < E2; ++e) {
+    const uint32_t i = e * 32 + lane;
+    uint64_t key = i < c ? b[i] : kDummyKey;
+    if (!key_is_dummy(key) && key_dist(key) <= bound) {
+      const uint32_t id = key_id(key);
+      const float* x = data + (size_t)id * ld;
+      float acc = 0.0f;
+      for (uint32_t d = 0; d < dim; ++d) acc = seq_step(acc, __ldg(x + d), __ldg(q + d));
+      w[e] = make_key(acc, id);
+      ++nre;
+    } else {
+      w[e] = kDummyKey;
+    }
+  }
+  // the band must fit the 256 re-rank slots
+  if (c > 32 * E2 && key_dist(b[32 * E2]) <= bound) over = true;
+  if (__any_sync(0xffffffffu, over)) {
+    if (lane == 0) fail_rows[atomicAdd(fail_cnt, 1u)] = row;
+    return;
+  }
+  warp_sort_regs<E2>(w, lane);
+#pragma unroll
+  for (int e = 0; e < E2; ++e) {
+    const uint32_t i = lane * E2 + e;
+    if (i < K) {
+      out_ids[(size_t)row * K + i] = key_id(w[e]);
+      out_dists[(size_t)row * K + i] = key_dist(w[e]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nre += __shfl_xor_sync(0xffffffffu, nre, o);
+  if (lane == 0 && reranked) atomicAdd(reranked, (unsigned long long)nre);
+}
+
+__global__ void gather_u16_rows_kernel(const uint16_t* __restrict__ src, uint32_t ld,
+                                       const uint32_t* __restrict__ rows, uint32_t cnt,
+                                       uint16_t* __restrict__ dst) {
+  uint32_t r = blockIdx.x;
+  if (r >= cnt) return;
+  const uint16_t* s = src + (size_t)rows[r] * ld;
+  for (uint32_t i = threadIdx.x; i < ld; i += blockDim.x) dst[(size_t)r * ld + i] = s[i];
+}
+
+__global__ void gather_f32_kernel(const float* __restrict__ src, const uint32_t* __restrict__ rows,
+                                  uint32_t cnt, float* __restrict__ dst) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) dst[i] = src[rows[i]];
+}
+
 __global__ void gather_rows_kernel(const float* __restrict__ src, uint32_t ld,
                                    const uint32_t* __restrict__ rows, uint32_t cnt,
                                    float* __restrict__ dst) {
@@ -554,10 +702,11 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp) {
+// rows x Kp bf16, consecutive rows `row_step` rows apart in memory
+CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_step) {
   CUtensorMap tm;
   cuuint64_t dims[2] = {Kp, rows};
-  cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)Kp * 2 * row_step};
   cuuint32_t box[2] = {TC_BK, TC_BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
@@ -570,7 +719,8 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp) {
 
 size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages) {
   return 1024 + (size_t)kblocks * TILE_BYTES + stages * TILE_BYTES +
-         sizeof(uint64_t) * (TC_PEND * TC_BM + 2 * stages + 1 + 2 * TC_ACC) + 16;
+         sizeof(uint64_t) * (TC_PEND * TC_BM + 2 * stages + 1 + 2 * TC_ACC) +
+         sizeof(float) * (TC_BM * 33 + 8) + 16;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -593,92 +743,232 @@ bool knn_tc_eligible(uint32_t dim, uint32_t K) {
          K + 32 + TC_PEND <= 256;
 }
 
+namespace {
+
+// Everything one kNN / top-k call shares between its passes.
+struct TcCall {
+  const float* data;
+  uint32_t n, ld, dim, K, Kp, kblocks, stages, dbg;
+  bool exclude_self;
+  float eps_rel, eps_norm;
+  const uint32_t* maxnorm;
+  const void* R;  // n x Kp bf16
+  cudaStream_t stream;
+};
+
+void run_tc_kernel(const TcCall& c, const CUtensorMap& tmA, const CUtensorMap& tmB, TcArgs a,
+                   uint32_t nq) {
+  a.kblocks = c.kblocks;
+  a.stages = c.stages;
+  a.dbg = c.dbg;
+  a.exclude_self = c.exclude_self ? 1 : 0;
+  a.nq = nq;
+  size_t smem = tc_smem_bytes(c.kblocks, c.stages);
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
+  CAGRA_LAUNCH_CHECK();
+}
+
+void dbg_report(const TcCall& c, const char* what, uint32_t nq) {
+  if (c.dbg != 3) return;
+  unsigned long long h[8];
+  CAGRA_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  CAGRA_CUDA_TRY(cudaMemcpyFromSymbol(h, g_tc_dbg, sizeof(h)));
+  fprintf(stderr,
+          "tc dbg [%s]: flush events %llu row-flushes %llu slow chunks %llu (warps %u) "
+          "cycles: flush %llu total %llu wait-tfull %llu\n",
+          what, h[0], h[1], h[3], (nq + 127) / 128 * 4, h[4], h[5], h[6]);
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  CAGRA_CUDA_TRY(cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)));
+}
+
+// Rows [0, nq) of the query side P (bf16, Kp wide; norms qnorm; fp32 rows
+// queries for the exact re-rank; self_ids for kNN rows) -> ids/dists [nq][K].
+// Single pass: running list of the K+32 smallest d~ per row.  Rows whose band
+// overflows go to the SIMT sequential-chain kernel.
+void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
+               const float* queries, uint32_t qld, const uint32_t* self_ids, uint32_t* ids,
+               float* dists, uint64_t& reranked, uint64_t& fallback) {
+  const uint32_t KC = c.K + 32;
+  Dev lists(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
+  CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, c.stream));
+  CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, c.stream));
+  CUtensorMap tmA = make_map(P, nq, c.Kp, 1), tmB = make_map(c.R, c.n, c.Kp, 1);
+  TcArgs a{};
+  a.n = c.n;
+  a.KC = KC;
+  a.mode = 0;
+  a.col_stride = 1;
+  a.lists = lists.as<uint64_t>();
+  a.self_ids = self_ids;
+  run_tc_kernel(c, tmA, tmB, a, nq);
+  dbg_report(c, "list", nq);
+  uint32_t* fail_cnt = fails.as<uint32_t>();
+  uint32_t* fail_rows = fail_cnt + 1;
+  tc_rerank_kernel<<<(nq + 7) / 8, 256, 0, c.stream>>>(
+      lists.as<uint64_t>(), nq, KC, c.K, qnorm, c.maxnorm, c.eps_rel, c.eps_norm, c.data, c.ld,
+      queries, qld, c.dim, ids, dists, fail_rows, fail_cnt, rer.as<unsigned long long>());
+  CAGRA_LAUNCH_CHECK();
+  uint32_t nf = 0;
+  unsigned long long nre = 0;
+  CAGRA_CUDA_TRY(cudaMemcpyAsync(&nf, fail_cnt, 4, cudaMemcpyDeviceToHost, c.stream));
+  CAGRA_CUDA_TRY(cudaMemcpyAsync(&nre, rer.p, 8, cudaMemcpyDeviceToHost, c.stream));
+  CAGRA_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  reranked += nre;
+  fallback += nf;
+  if (!nf) return;
+  // exact SIMT kernel for the rows whose candidate band overflowed
+  Dev q((size_t)nf * qld * 4), sid(4ull * nf), sc(8ull * nf * c.K), fi(4ull * nf * c.K),
+      fd(4ull * nf * c.K);
+  gather_rows_kernel<<<nf, 128, 0, c.stream>>>(queries, qld, fail_rows, nf, q.as<float>());
+  CAGRA_LAUNCH_CHECK();
+  const uint32_t* simt_self = nullptr;
+  if (c.exclude_self) {
+    if (self_ids) {
+      gather_f32_kernel<<<(nf + 255) / 256, 256, 0, c.stream>>>(
+          reinterpret_cast<const float*>(self_ids), fail_rows, nf, sid.as<float>());
+      CAGRA_LAUNCH_CHECK();
+      simt_self = sid.as<uint32_t>();
+    } else {
+      simt_self = fail_rows;
+    }
+  }
+  launch_exact_topk_simt(c.data, c.n, c.ld, q.as<float>(), nf, qld, c.dim, c.K, c.exclude_self,
+                         simt_self, sc.as<uint64_t>(), fi.as<uint32_t>(), fd.as<float>(),
+                         c.stream);
+  scatter_rows_kernel<<<nf, 128, 0, c.stream>>>(fail_rows, nf, c.K, fi.as<uint32_t>(),
+                                                fd.as<float>(), ids, dists);
+  CAGRA_LAUNCH_CHECK();
+  CAGRA_CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+
+constexpr uint32_t kSampleStride = 16;
+
+}  // namespace
+
 void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
                    uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
   if (nq == 0) return;
-  const uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK), kblocks = Kp / TC_BK;
-  const uint32_t KC = K + 32;  // list size (dummy keys pad inputs with fewer points)
+  TcCall c;
+  c.data = d_data;
+  c.n = n;
+  c.ld = ld;
+  c.dim = dim;
+  c.K = K;
+  c.Kp = round_up_u32(3 * dim + 6, TC_BK);
+  c.kblocks = c.Kp / TC_BK;
+  c.stages = tc_stages(c.kblocks);
+  const char* dbg = std::getenv("CAGRA_TC_DEBUG");
+  c.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
+  c.exclude_self = exclude_self;
+  c.stream = stream;
+  // error bound of d~ (file header): |d~ - d| <= eps_rel |q| max|x| +
+  // eps_norm (|q|^2 + max|x|^2): the split's omitted terms (3.1*2^-16 of
+  // sum|q_i||x_i| <= |q||x|, doubled by the -2), fp32 accumulation over Kp
+  // terms of total magnitude 2|q||x| + |q|^2 + |x|^2, and the fp32 norms.
+  const float u23 = 1.1920929e-07f;
+  c.eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)c.Kp * u23;
+  c.eps_norm = (float)c.Kp * u23 + (float)(dim + 8) * u23;
+
   const bool same = exclude_self;  // kNN graph: queries are the data rows
-  Dev dP((size_t)nq * Kp * 2), dR((size_t)n * Kp * 2), dqn(4ull * nq),
-      dxn(4ull * n), dmax(4), lists(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
+  Dev dP((size_t)nq * c.Kp * 2), dR((size_t)n * c.Kp * 2), dqn(4ull * nq), dxn(4ull * n), dmax(4);
   CAGRA_CUDA_TRY(cudaMemsetAsync(dmax.p, 0, 4, stream));
-  CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, stream));
-  CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
   // data side: R (and P when the queries are the data), norms, max norm
-  tc_split_kernel<<<(n + 7) / 8, 256, 0, stream>>>(d_data, n, ld, dim, Kp,
+  tc_split_kernel<<<(n + 7) / 8, 256, 0, stream>>>(d_data, n, ld, dim, c.Kp,
                                                    same ? dP.as<__nv_bfloat16>() : nullptr,
                                                    dR.as<__nv_bfloat16>(), dxn.as<float>(),
                                                    dmax.as<uint32_t>());
   CAGRA_LAUNCH_CHECK();
   const float* qnorm = dxn.as<float>();
   if (!same) {
-    tc_split_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(d_queries, nq, qld, dim, Kp,
+    tc_split_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(d_queries, nq, qld, dim, c.Kp,
                                                       dP.as<__nv_bfloat16>(), nullptr,
                                                       dqn.as<float>(), nullptr);
     CAGRA_LAUNCH_CHECK();
     qnorm = dqn.as<float>();
   }
-  CUtensorMap tmA = make_map(dP.p, nq, Kp), tmB = make_map(dR.p, n, Kp);
-  TcArgs a;
-  a.nq = nq;
-  a.n = n;
-  a.kblocks = kblocks;
-  a.KC = KC;
-  a.exclude_self = exclude_self ? 1 : 0;
-  a.lists = lists.as<uint64_t>();
-  a.stages = tc_stages(kblocks);
-  const char* dbg = std::getenv("CAGRA_TC_DEBUG");
-  a.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
-  size_t smem = tc_smem_bytes(kblocks, a.stages);
-  CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, stream>>>(tmA, tmB, a);
-  CAGRA_LAUNCH_CHECK();
-  // error bound of d~ (file header): |d~ - d| <= eps_rel |q| max|x| +
-  // eps_norm (|q|^2 + max|x|^2): the split's omitted terms (3.1*2^-16 of
-  // sum|q_i||x_i| <= |q||x|, doubled by the -2), fp32 accumulation over Kp
-  // terms of total magnitude 2|q||x| + |q|^2 + |x|^2, and the fp32 norms.
-  const float u23 = 1.1920929e-07f;
-  const float eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)Kp * u23;
-  const float eps_norm = (float)Kp * u23 + (float)(dim + 8) * u23;
-  uint32_t* fail_rows = fails.as<uint32_t>() + 1;
-  uint32_t* fail_cnt = fails.as<uint32_t>();
-  tc_rerank_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
-      lists.as<uint64_t>(), nq, KC, K, qnorm, dmax.as<uint32_t>(), eps_rel, eps_norm, d_data, ld,
-      d_queries, qld, dim, d_ids, d_dists, fail_rows, fail_cnt,
-      rer.as<unsigned long long>());
-  CAGRA_LAUNCH_CHECK();
-  if (a.dbg == 3) {
-    unsigned long long h[8];
-    CAGRA_CUDA_TRY(cudaMemcpyFromSymbol(h, g_tc_dbg, sizeof(h)));
-    fprintf(stderr, "tc dbg: flush events %llu row-flushes %llu keys flushed %llu slow chunks %llu"
-                    " (warps %u) cycles: flush %llu total %llu wait-tfull %llu\n", h[0], h[1], h[2],
-            h[3], (nq + 127) / 128 * 4, h[4], h[5], h[6]);
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    CAGRA_CUDA_TRY(cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)));
-  }
-  uint32_t nf = 0;
-  unsigned long long nre = 0;
-  CAGRA_CUDA_TRY(cudaMemcpyAsync(&nf, fail_cnt, 4, cudaMemcpyDeviceToHost, stream));
-  CAGRA_CUDA_TRY(cudaMemcpyAsync(&nre, rer.p, 8, cudaMemcpyDeviceToHost, stream));
-  CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
-  g_knn_tc_stats.rows = nq;
-  g_knn_tc_stats.fallback_rows = nf;
-  g_knn_tc_stats.reranked = nre;
-  if (nf) {
-    // exact SIMT kernel for the rows whose candidate band overflowed
-    Dev q((size_t)nf * qld * 4), sc(8ull * nf * K), fi(4ull * nf * K), fd(4ull * nf * K);
-    gather_rows_kernel<<<nf, 128, 0, stream>>>(d_queries, qld, fail_rows, nf, q.as<float>());
+  c.maxnorm = dmax.as<uint32_t>();
+  c.R = dR.p;
+  uint64_t reranked = 0, fallback = 0, retried = 0;
+
+  const char* onepass = std::getenv("CAGRA_TC_ONEPASS");
+  const bool two_pass = n / kSampleStride >= 4096 && !(onepass && onepass[0] == '1');
+  if (!two_pass) {
+    list_pass(c, dP.p, nq, qnorm, d_queries, qld, nullptr, d_ids, d_dists, reranked, fallback);
+  } else {
+    // pass 1: every 16th point; the r-th smallest d~ over the sample is an
+    // upper bound of the r-th smallest over all points (valid for ANY r).
+    const uint32_t ns = n / kSampleStride;
+    const uint32_t r = std::max<uint32_t>(8, (3 * (K + 16) + kSampleStride - 1) / kSampleStride);
+    const uint32_t capg = (uint64_t)nq * 1024 * 8 <= (8ull << 30) ? 1024 : 512;
+    Dev lists1(8ull * r * nq), bufs(8ull * nq * capg), bcount(4ull * nq), fails(4ull * nq + 4),
+        rer(8);
+    CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, stream));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
+    CUtensorMap tmA = make_map(dP.p, nq, c.Kp, 1);
+    CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride);
+    CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1);
+    TcArgs a{};
+    a.n = ns;
+    a.KC = r;
+    a.mode = 0;
+    a.col_stride = kSampleStride;
+    a.lists = lists1.as<uint64_t>();
+    run_tc_kernel(c, tmA, tmS, a, nq);
+    dbg_report(c, "sample", nq);
+    // pass 2: every point with d~ <= tau* appended (no merging)
+    TcArgs b{};
+    b.n = n;
+    b.KC = r;
+    b.mode = 1;
+    b.col_stride = 1;
+    b.tau_keys = lists1.as<uint64_t>();
+    b.tau_ld = r;
+    b.bufs = bufs.as<uint64_t>();
+    b.bcount = bcount.as<uint32_t>();
+    b.capg = capg;
+    run_tc_kernel(c, tmA, tmB, b, nq);
+    dbg_report(c, "append", nq);
+    uint32_t* fail_cnt = fails.as<uint32_t>();
+    uint32_t* fail_rows = fail_cnt + 1;
+    tc_rerank_append_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
+        bufs.as<uint64_t>(), bcount.as<uint32_t>(), capg, lists1.as<uint64_t>(), r, nq, K, qnorm,
+        c.maxnorm, c.eps_rel, c.eps_norm, d_data, ld, d_queries, qld, dim, d_ids, d_dists,
+        fail_rows, fail_cnt, rer.as<unsigned long long>());
     CAGRA_LAUNCH_CHECK();
-    launch_exact_topk_simt(d_data, n, ld, q.as<float>(), nf, qld, dim, K, exclude_self,
-                           exclude_self ? fail_rows : nullptr, sc.as<uint64_t>(),
-                           fi.as<uint32_t>(), fd.as<float>(), stream);
-    scatter_rows_kernel<<<nf, 128, 0, stream>>>(fail_rows, nf, K, fi.as<uint32_t>(),
-                                                fd.as<float>(), d_ids, d_dists);
-    CAGRA_LAUNCH_CHECK();
+    uint32_t nf = 0;
+    unsigned long long nre = 0;
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(&nf, fail_cnt, 4, cudaMemcpyDeviceToHost, stream));
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(&nre, rer.p, 8, cudaMemcpyDeviceToHost, stream));
     CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
+    reranked += nre;
+    retried = nf;
+    if (nf) {
+      // the rows whose threshold did not bracket their band: single-pass list
+      // mode on just those rows
+      Dev P2((size_t)nf * c.Kp * 2), qn2(4ull * nf), q2((size_t)nf * qld * 4), ids2(4ull * nf * K),
+          d2(4ull * nf * K);
+      gather_u16_rows_kernel<<<nf, 128, 0, stream>>>(dP.as<uint16_t>(), c.Kp, fail_rows, nf,
+                                                     P2.as<uint16_t>());
+      gather_f32_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(qnorm, fail_rows, nf,
+                                                              qn2.as<float>());
+      gather_rows_kernel<<<nf, 128, 0, stream>>>(d_queries, qld, fail_rows, nf, q2.as<float>());
+      CAGRA_LAUNCH_CHECK();
+      list_pass(c, P2.p, nf, qn2.as<float>(), q2.as<float>(), qld,
+                exclude_self ? fail_rows : nullptr, ids2.as<uint32_t>(), d2.as<float>(), reranked,
+                fallback);
+      scatter_rows_kernel<<<nf, 128, 0, stream>>>(fail_rows, nf, K, ids2.as<uint32_t>(),
+                                                  d2.as<float>(), d_ids, d_dists);
+      CAGRA_LAUNCH_CHECK();
+      CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
+    }
   }
+  g_knn_tc_stats.rows = nq;
+  g_knn_tc_stats.fallback_rows = fallback;
+  g_knn_tc_stats.reranked = reranked;
+  g_knn_tc_stats.retried_rows = retried;
 }
 
 }  // namespace cagra

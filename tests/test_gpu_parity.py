@@ -75,6 +75,50 @@ def test_knn_odd_dimension_and_ragged_tiles(gpu, oracle):
         assert np.array_equal(bits(knn.dists), bits(ref_d))
 
 
+@pytest.mark.parametrize("n,dim,k,two_pass", [
+    (3000, 128, 64, False),    # single pass, D=128 (7 K-blocks, 3-stage ring)
+    (70000, 96, 128, True),    # sample pass + append pass (DEEP shape, d_init 128)
+    (90000, 37, 40, True),     # odd dim, ragged last tile
+])
+def test_knn_tensor_core_path_bit_exact(gpu, oracle, monkeypatch, n, dim, k, two_pass):
+    # K1 on tcgen05 (knn_tc.cu) against the SIMT sequential-chain kernel (itself
+    # bit-exact vs the reference above) and, on the small case, the oracle.
+    data = oracle.uniform_dataset(n, dim, 1000 + n)
+    ds = fodg.Dataset.from_array(data)
+    monkeypatch.setenv("CAGRA_KNN_PATH", "auto")
+    tc = fodg.exact_knn_graph(ds, k)
+    st = capi.knn_last_stats()
+    assert st["rows"] == n and st["reranked"] >= n * k, st   # the tensor-core path ran
+    queries = oracle.uniform_dataset(500, dim, 77)
+    gt_tc = fodg.exact_topk_batch(ds, queries, 10)
+    monkeypatch.setenv("CAGRA_KNN_PATH", "simt")
+    simt = fodg.exact_knn_graph(ds, k)
+    assert capi.knn_last_stats()["rows"] == 0
+    gt_simt = fodg.exact_topk_batch(ds, queries, 10)
+    assert np.array_equal(tc.ids, simt.ids)
+    assert np.array_equal(bits(tc.dists), bits(simt.dists))
+    assert np.array_equal(gt_tc[0], gt_simt[0])
+    assert np.array_equal(bits(gt_tc[1]), bits(gt_simt[1]))
+    if n <= 5000:
+        ref_ids, ref_d = oracle.exact_knn_graph(data, k)
+        assert np.array_equal(tc.ids, ref_ids)
+        assert np.array_equal(bits(tc.dists), bits(ref_d))
+
+
+def test_knn_tensor_core_single_pass_forced(gpu, oracle, monkeypatch):
+    # the single-pass list mode (used for retried rows) on a size that would
+    # normally take two passes
+    data = oracle.uniform_dataset(70000, 24, 5)
+    ds = fodg.Dataset.from_array(data)
+    monkeypatch.setenv("CAGRA_KNN_PATH", "auto")
+    monkeypatch.setenv("CAGRA_TC_ONEPASS", "1")
+    one = fodg.exact_knn_graph(ds, 32)
+    monkeypatch.delenv("CAGRA_TC_ONEPASS")
+    two = fodg.exact_knn_graph(ds, 32)
+    assert np.array_equal(one.ids, two.ids)
+    assert np.array_equal(bits(one.dists), bits(two.dists))
+
+
 # ------------------------------------------------------------ optimize ----
 @pytest.mark.parametrize("name", CORPORA)
 def test_optimize_stages_bit_exact(gpu, oracle, name):
