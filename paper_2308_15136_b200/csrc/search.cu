@@ -33,6 +33,8 @@
 // re-scored with the sequential chain and re-sorted, so reported distances are
 // always bit-equal to the reference's.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -58,6 +60,7 @@ struct KParams {
   const float* data;
   const uint32_t* graph;
   uint32_t n, dim, ld, degree;
+  uint32_t deg_shift;  // log2(degree) when a power of two, else 0xff
   const float* queries;
   uint32_t nq;
   uint32_t k, M, p, C, max_iter, min_iter, policy, reset_interval;
@@ -72,7 +75,12 @@ struct KParams {
   uint32_t* out_counts;
   DevStats* stats;
   int* error;
+  unsigned long long* prof;  // optional phase cycle counters (CAGRA_SEARCH_PROF)
 };
+
+#define PROF_T(var) long long var = (P.prof && threadIdx.x == 0) ? clock64() : 0
+#define PROF_ADD(slot, since) \
+  do { if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[slot], (unsigned long long)(clock64() - since)); } while (0)
 
 // ------------------------------------------------------------- init ids ----
 __global__ void init_samples_kernel(uint32_t nq, uint32_t C, uint32_t teams, uint32_t n,
@@ -139,6 +147,76 @@ __device__ void block_sort_smem(uint64_t* a, uint32_t P) {
   }
 }
 
+// Block-wide bitonic sort of a[0..EPT*SNT) held EPT keys per thread in
+// registers (index = tid*EPT + e): intra-thread and intra-warp stages need no
+// barrier; only partner distances >= 32*EPT go through shared memory (6
+// barrier pairs for 1024 keys instead of 55 barriers).  a is used as the
+// exchange buffer and holds the sorted keys on return (caller syncs before).
+template <int EPT>
+__device__ void block_sort_regs(uint64_t* a) {
+  constexpr uint32_t P = EPT * SNT;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  uint64_t v[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) v[e] = a[tid * EPT + e];
+#pragma unroll
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j < (uint32_t)EPT) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if ((e & j) == 0) {
+            const uint32_t i = tid * EPT + e;
+            const bool up = (i & k) == 0;
+            uint64_t x = v[e], y = v[e ^ j];
+            if ((x > y) == up) {
+              v[e] = y;
+              v[e ^ j] = x;
+            }
+          }
+        }
+      } else if (j < 32u * EPT) {
+        const uint32_t lm = j / EPT;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const uint32_t i = tid * EPT + e;
+          const bool up = (i & k) == 0, lower = (lane & lm) == 0;
+          uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], lm);
+          uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) a[tid * EPT + e] = v[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const uint32_t i = tid * EPT + e;
+          const bool up = (i & k) == 0, lower = (i & j) == 0;
+          uint64_t o = a[i ^ j];
+          uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) a[tid * EPT + e] = v[e];
+}
+
+// a[0..P) for P a power of two in [256, 2048] via the register sort, else the
+// smem network.
+__device__ __noinline__ void block_sort_any(uint64_t* a, uint32_t P) {
+  if (P == 256) block_sort_regs<1>(a);
+  else if (P == 512) block_sort_regs<2>(a);
+  else if (P == 1024) block_sort_regs<4>(a);
+  else if (P == 2048) block_sort_regs<8>(a);
+  else block_sort_smem(a, P);
+}
+
 // #{i < len : cmp_key(a[i]) < key}   (a sorted by cmp_key)
 __device__ __forceinline__ uint32_t lb_cmp(const uint64_t* a, uint32_t len, uint64_t key) {
   uint32_t lo = 0, hi = len;
@@ -148,6 +226,20 @@ __device__ __forceinline__ uint32_t lb_cmp(const uint64_t* a, uint32_t len, uint
     else hi = mid;
   }
   return lo;
+}
+
+// Warp-aggregated append: every lane with `pred` gets a distinct slot of the
+// shared counter `*ctr` (one atomic per warp instead of one per element).
+// Must be called by all 32 lanes of the warp.
+__device__ __forceinline__ uint32_t warp_append_slot(uint32_t* ctr, bool pred) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return 0;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(ctr, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
 }
 
 // ------------------------------------------------------------ visited -----
@@ -233,12 +325,21 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
                                           uint32_t nev, uint32_t SP) {
   const int tid = threadIdx.x;
   if (EXACT) {
-    for (uint32_t e = tid; e < nev; e += SNT) {
-      uint32_t id = S.evlist[e];
-      uint32_t t = S.evteam[e];
-      float dist = exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim);
-      uint64_t key = make_key(dist, id);
-      if (key < ctl.worst[t]) {
+    for (uint32_t e0 = 0; e0 < nev; e0 += SNT) {
+      const uint32_t e = e0 + tid;
+      uint64_t key = kDummyKey;
+      uint32_t t = 0;
+      if (e < nev) {
+        uint32_t id = S.evlist[e];
+        t = S.evteam[e];
+        float dist = exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim);
+        key = make_key(dist, id);
+      }
+      const bool keep = e < nev && key < ctl.worst[t];
+      if (P.teams == 1) {
+        const uint32_t pos = warp_append_slot(&ctl.nsurv[0], keep);
+        if (keep) S.surv[pos] = key;
+      } else if (keep) {
         uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
         S.surv[t * SP + pos] = key;
       }
@@ -253,7 +354,8 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
       uint32_t ch = lt + TEAM * c;
       qr[c] = ch < nchunk ? reinterpret_cast<const float4*>(S.q)[ch] : make_float4(0, 0, 0, 0);
     }
-    constexpr int U = 2;  // rows in flight per team
+    // rows in flight per team (register budget ~9-12 float4 per lane)
+    constexpr int U = MAXC <= 2 ? 4 : (MAXC == 3 ? 3 : 2);
     // warp-uniform trip count: every lane runs every iteration (the team
     // shuffles below use the full mask)
     for (uint32_t base = 0; base < nev; base += NTEAMS * U) {
@@ -285,14 +387,21 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
 #pragma unroll
         for (int o = TEAM / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, TEAM);
         uint32_t e = e0 + u * NTEAMS;
+        uint64_t key = kDummyKey;
+        uint32_t t = 0;
+        bool keep = false;
         if (lt == 0 && e < nev) {
           uint32_t id = S.evlist[e];
-          uint32_t t = S.evteam[e];
-          uint64_t key = make_key(acc, id);
-          if (key < ctl.worst[t]) {
-            uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
-            S.surv[t * SP + pos] = key;
-          }
+          t = S.evteam[e];
+          key = make_key(acc, id);
+          keep = key < ctl.worst[t];
+        }
+        if (P.teams == 1) {
+          const uint32_t pos = warp_append_slot(&ctl.nsurv[0], keep);
+          if (keep) S.surv[pos] = key;
+        } else if (keep) {
+          uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
+          S.surv[t * SP + pos] = key;
         }
       }
     }
@@ -436,7 +545,7 @@ search_kernel(const KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Ctl ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t SP = next_pow2_u32(P.C);
+  const uint32_t SP = max(256u, next_pow2_u32(P.C));  // survivor buffer (block sort pads to 256)
   Smem S;
   {
     unsigned char* p = smem_raw;
@@ -490,23 +599,45 @@ search_kernel(const KParams P) {
 
     // visit(): candidates [src 0..cnt) -> evlist of first visits
     auto visit = [&](const uint32_t* src_ids, bool from_graph, uint32_t cnt) {
+      PROF_T(tv0);
       bool slow = forget && (ctl.count + cnt > P.hcap);
       if (!slow) {
         if (tid == 0) ctl.nev = 0;
         __syncthreads();
-        for (uint32_t j = tid; j < cnt; j += SNT) {
-          uint32_t id;
-          if (from_graph) {
-            uint32_t pi = j / P.degree, c = j - pi * P.degree;
-            id = __ldg(&P.graph[(size_t)S.parents[pi] * P.degree + c]);
-          } else {
-            id = __ldg(&src_ids[j]);
+        // all of this thread's candidate ids are loaded before any insert, so
+        // the graph-row gathers overlap instead of queueing behind the atomics
+        constexpr int VPT = 8;
+        for (uint32_t j0 = 0; j0 < cnt; j0 += SNT * VPT) {
+          uint32_t ids[VPT];
+#pragma unroll
+          for (int k = 0; k < VPT; ++k) {
+            const uint32_t j = j0 + k * SNT + tid;
+            ids[k] = 0;
+            if (j < cnt) {
+              if (from_graph) {
+                const uint32_t pi = j >> P.deg_shift, c = j & (P.degree - 1);
+                ids[k] = P.deg_shift != 0xffu
+                             ? __ldg(&P.graph[(size_t)S.parents[pi] * P.degree + c])
+                             : __ldg(&P.graph[(size_t)S.parents[j / P.degree] * P.degree +
+                                              j % P.degree]);
+              } else {
+                ids[k] = __ldg(&src_ids[j]);
+              }
+            }
           }
-          bool ins = SMEM_TABLE ? smem_insert(S.table, mask, id) : gtab_insert(gtab, mask, tag, id);
-          if (ins) {
-            uint32_t pos = atomicAdd(&ctl.nev, 1u);
-            S.evlist[pos] = id;
-            S.evteam[pos] = 0;
+#pragma unroll
+          for (int k = 0; k < VPT; ++k) {
+            const uint32_t j = j0 + k * SNT + tid;
+            if (j0 + k * SNT >= cnt) break;
+            bool ins = false;
+            if (j < cnt)
+              ins = SMEM_TABLE ? smem_insert(S.table, mask, ids[k])
+                               : gtab_insert(gtab, mask, tag, ids[k]);
+            const uint32_t pos = warp_append_slot(&ctl.nev, ins);
+            if (ins) {
+              S.evlist[pos] = ids[k];
+              S.evteam[pos] = 0;
+            }
           }
         }
         __syncthreads();
@@ -535,11 +666,14 @@ search_kernel(const KParams P) {
         if (!SMEM_TABLE) tag = ctl.slow;
       }
       __syncthreads();
+      PROF_ADD(0, tv0);
+      PROF_T(te0);
       uint32_t nev = ctl.nev;
       if (MAXC > 0) eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT>(P, S, ctl, nev, SP);
       else eval_list_generic<EXACT>(P, S, ctl, nev, SP);
       if (tid == 0) ctl.evals[0] += nev;
       __syncthreads();
+      PROF_ADD(1, te0);
     };
 
     // update_topm(): merge survivors into top
@@ -555,13 +689,13 @@ search_kernel(const KParams P) {
           }
           __syncthreads();
         }
-        if (ns <= 256) {
+        if (ns <= 64) {
           if (warp == 0) warp_sort_smem(S.surv, ns, lane);
         } else {
-          uint32_t P2 = next_pow2_u32(ns);
+          const uint32_t P2 = max(256u, next_pow2_u32(ns));
           for (uint32_t j = ns + tid; j < P2; j += SNT) S.surv[j] = kDummyKey;
           __syncthreads();
-          block_sort_smem(S.surv, P2);
+          block_sort_any(S.surv, P2);
         }
         __syncthreads();
         if (ctl.dup) {
@@ -626,8 +760,13 @@ search_kernel(const KParams P) {
     for (;;) {
       // ---- step (search.cpp:218-245)
       DBG("q%u it%u merge ns=%u\n", qi, iters, ctl.nsurv[0]);
-      merge();
+      {
+        PROF_T(tm0);
+        merge();
+        PROF_ADD(2, tm0);
+      }
       DBG("q%u it%u merged\n", qi, iters);
+      PROF_T(ts0);
       pending = false;
       ++iters;
       // select_parents: first p unflagged non-dummy entries
@@ -658,6 +797,7 @@ search_kernel(const KParams P) {
         __syncthreads();
       }
       uint32_t np = ctl.npar[0];
+      PROF_ADD(3, ts0);
       DBG("q%u it%u np=%u\n", qi, iters, np);
       if (np == 0) {
         converged = iters >= P.min_iter;
@@ -669,8 +809,10 @@ search_kernel(const KParams P) {
       visit(nullptr, true, np * P.degree);
       pending = true;
       if (forget && iters % P.reset_interval == 0) {
+        PROF_T(tr0);
         table_reset<SMEM_TABLE>(P, S, ctl, top, gtab, tag);
         if (tid == 0) ctl.resets++;
+        PROF_ADD(4, tr0);
       }
       if (iters >= P.max_iter) break;
     }
@@ -702,7 +844,7 @@ search_kernel(const KParams P) {
         uint32_t P2 = next_pow2_u32(live);
         for (uint32_t j = live + tid; j < P2; j += SNT) nxt[j] = kDummyKey;
         __syncthreads();
-        block_sort_smem(nxt, P2);
+        block_sort_any(nxt, P2);
       }
       __syncthreads();
       top = nxt;
@@ -1026,7 +1168,7 @@ struct Variant {
 
 Variant pick_variant(uint32_t ld, uint32_t req_team) {
   uint32_t ch = ld / 4;
-  const Variant table[] = {{4, 2}, {8, 4}, {16, 4}, {32, 8}};
+  const Variant table[] = {{4, 2}, {8, 3}, {8, 4}, {16, 4}, {32, 8}};
   for (const Variant& v : table) {
     if (req_team && (uint32_t)v.team != req_team) continue;
     if ((uint32_t)(v.team * v.maxc) >= ch) return v;
@@ -1041,6 +1183,7 @@ KernelFn per_query_fn(Variant v) {
   if (EXACT) return search_kernel<32, 1, true, SMEM>;
   switch (v.team * 100 + v.maxc) {
     case 402: return search_kernel<4, 2, false, SMEM>;
+    case 803: return search_kernel<8, 3, false, SMEM>;
     case 804: return search_kernel<8, 4, false, SMEM>;
     case 1604: return search_kernel<16, 4, false, SMEM>;
     case 3208: return search_kernel<32, 8, false, SMEM>;
@@ -1052,6 +1195,7 @@ KernelFn shared_fn(bool exact, Variant v) {
   if (exact) return shared_search_kernel<32, 1, true>;
   switch (v.team * 100 + v.maxc) {
     case 402: return shared_search_kernel<4, 2, false>;
+    case 803: return shared_search_kernel<8, 3, false>;
     case 804: return shared_search_kernel<8, 4, false>;
     case 1604: return shared_search_kernel<16, 4, false>;
     case 3208: return shared_search_kernel<32, 8, false>;
@@ -1093,7 +1237,7 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   const uint32_t ldr = round_up_u32(ix.ld, 4);
   size_t smem;
   if (!shared) {
-    uint32_t SP = next_pow2_u32(C);
+    uint32_t SP = std::max(256u, next_pow2_u32(C));
     smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * C + 2ull * round_up_u32(C, 2) +
            4ull * round_up_u32(p, 4) + (pl.smem_table ? 4ull * hcap : 0);
   } else {
@@ -1151,6 +1295,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.dim = ix.dim;
   P.ld = ix.ld;
   P.degree = ix.degree;
+  P.deg_shift = (ix.degree & (ix.degree - 1)) == 0 ? (uint32_t)__builtin_ctz(ix.degree) : 0xffu;
   P.queries = d_queries;
   P.nq = nq;
   P.k = c.k;
@@ -1172,9 +1317,28 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.out_counts = d_counts;
   P.stats = reinterpret_cast<DevStats*>(d_stats);
   P.error = nullptr;
+  P.prof = nullptr;
+  const char* penv = std::getenv("CAGRA_SEARCH_PROF");
+  static unsigned long long* d_prof = nullptr;
+  if (penv && penv[0] == '1') {
+    if (!d_prof) CAGRA_CUDA_TRY(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), stream));
+    P.prof = d_prof;
+  }
   KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(pl.fn));
   fn<<<pl.grid, SNT, pl.smem, stream>>>(P);
   CAGRA_LAUNCH_CHECK();
+  if (P.prof) {
+    unsigned long long h[8];
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
+    double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
+    fprintf(stderr, "search prof (cycles summed over CTAs, grid %u): visit %.3g eval %.3g merge %.3g "
+                    "select %.3g reset %.3g | shares %.1f%% %.1f%% %.1f%% %.1f%% %.1f%%\n",
+            pl.grid, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4],
+            100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot,
+            100 * h[4] / tot);
+  }
   return 2;
 }
 

@@ -48,20 +48,19 @@ def main():
     grid = []
     if args.grid:
         for tok in args.grid.split(";"):
-            m, p, pol, bits, ts = (tok.split(",") + ["0", "0", "0"])[:5]
-            grid.append((int(m), int(p), int(pol), int(bits), int(ts)))
+            m, p, pol, bits, ts, ri = (tok.split(",") + ["0", "0", "0", "1"])[:6]
+            grid.append((int(m), int(p), int(pol), int(bits), int(ts), int(ri)))
     else:
         for m, p in [(512, 8), (768, 16), (896, 16), (1024, 16), (1024, 32)]:
             for pol in (0, 1):
                 for ts in (4, 8, 16):
-                    grid.append((m, p, pol, 0, ts))
-    for (m, p, pol, bits, ts) in grid:
+                    grid.append((m, p, pol, 0, ts, 1))
+    for (m, p, pol, bits, ts, ri) in grid:
         if not bits:
             need = m + p * args.d
             bits = max(10, int(np.ceil(np.log2(need * 1.6))))
         prm = fodg.SearchParams(k=10, topm=m, width=p, hash_policy=fodg.HashPolicy(pol),
-                                hash_bits=bits, seed=11,
-                                max_iterations=max(16, 2 * m // p + 16))
+                                hash_bits=bits, seed=11, reset_interval=ri)
         opt = fodg.EngineOptions(team_size=ts)
         try:
             ix.search_dev(qd, args.nq, prm, opt, ids, dists, None, stats, stream)
@@ -85,7 +84,7 @@ def main():
         rec = np.mean([len(set(hid[i]) & set(gt[i])) / 10 for i in range(args.nq)])
         bytes_q = evals.mean() * args.dim * 4 + iters.mean() * p * args.d * 4
         gbs = bytes_q * args.nq / (ms * 1e-3) / 1e9
-        print(f"M={m:5d} p={p:3d} pol={pol} bits={bits:2d} ts={ts} recall={rec:.4f} "
+        print(f"M={m:5d} p={p:3d} pol={pol} bits={bits:2d} ts={ts} ri={ri} recall={rec:.4f} "
               f"qps={args.nq / (ms * 1e-3):10.0f} ms={ms:8.2f} evals={evals.mean():8.0f} "
               f"iters={iters.mean():6.1f} alg_GBs={gbs:7.0f}", flush=True)
 
