@@ -62,8 +62,10 @@ def parse():
     ap.add_argument("--hash-bits", type=int, default=12)
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="queries in the CPU baseline sample (0 = auto, ~10-30 s of work)")
-    ap.add_argument("--batch1", type=int, default=0,
+    ap.add_argument("--batch1", type=int, default=500,
                     help="also time this many sequential batch-1 calls (0 = off)")
+    ap.add_argument("--b1-topm", type=int, default=16, help="batch-1 team top-M")
+    ap.add_argument("--b1-teams", type=int, default=64, help="batch-1 teams (one CTA each)")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -350,21 +352,22 @@ def run_ours(args):
     e2e_ids = h_ids.numpy().view(np.uint32)
     assert np.array_equal(e2e_ids, hid), "device-resident and host-buffer paths disagree"
 
-    # ---- optional batch-1 latency path (sequential single-query calls)
+    # ---- batch-1 path: sequential single-query calls through the C ABI (host
+    # buffers), shared mode as choose_mode picks for batch 1 (engine.cpp:86-93),
+    # one CTA per team (multi-CTA)
     b1 = None
     if args.batch1:
-        nb = args.batch1
-        pc1 = prm.c()
-        mode = fodg.choose_mode(1, args.topm)
-        oc1 = opt.c(0, qoff)
-        oc1.mode = int(mode)
-        oc1.team_count = 4
+        nb = min(args.batch1, nq)
+        prm1 = fodg.SearchParams(k=10, topm=args.b1_topm, width=1, seed=11)
+        mode = fodg.choose_mode(1, args.b1_topm)
+        opt1 = fodg.EngineOptions(device=local, mode=mode, team_count=args.b1_teams)
+        pc1, oc1 = prm1.c(), opt1.c(0, qoff)
         one_i = torch.empty((1, k), dtype=torch.int32).pin_memory()
         one_d = torch.empty((1, k), dtype=torch.float32).pin_memory()
         out = np.empty((nb, k), np.uint32)
         for i in range(min(3, nb)):
-            L.cagra_search(ix.h, capi.ptr(hq[i]), 1, args.dim, C.byref(pc1), C.byref(oc1),
-                           capi.ptr(one_i), capi.ptr(one_d), None, None)
+            capi.check(L.cagra_search(ix.h, capi.ptr(hq[i]), 1, args.dim, C.byref(pc1),
+                                      C.byref(oc1), capi.ptr(one_i), capi.ptr(one_d), None, None))
         t0 = time.perf_counter()
         for i in range(nb):
             capi.check(L.cagra_search(ix.h, capi.ptr(hq[i]), 1, args.dim, C.byref(pc1),
@@ -372,8 +375,10 @@ def run_ours(args):
                                       None))
             out[i] = one_i.numpy().view(np.uint32)[0]
         b1s = time.perf_counter() - t0
-        b1 = {"qps": nb / b1s, "recall@10": recall_at_k(out, gt[:nb]), "queries": nb,
-              "mode": fodg.mode_name(mode)}
+        b1 = {"qps": nb / b1s, "latency_us": b1s / nb * 1e6, "recall@10": recall_at_k(out, gt[:nb]),
+              "queries": nb, "mode": fodg.mode_name(mode), "team_topm": args.b1_topm,
+              "teams": args.b1_teams, "launches_per_query": ix.last_launch_count(),
+              "path": "C-ABI cagra_search, pinned host buffers, one CTA per team"}
 
     # ---- max over ranks
     vals = torch.tensor([total_ms, e2e_s, kernel_ms], dtype=torch.float64, device=dev)

@@ -92,6 +92,11 @@ typedef struct cagra_engine_opts {
                                to the CPU; 0: warp-team reduction (faster),
                                final k re-scored with the sequential chain */
   uint32_t team_size;     /* lanes per distance in fast mode: 0=auto,4,8,16,32 */
+  uint32_t multi_cta;     /* shared mode: 0 auto (one CTA per team when the batch
+                             is smaller than the SM count and exact_distances=0),
+                             1 single-CTA lockstep teams (the reference's team
+                             order, engine.cpp:63-72), 2 one CTA per team */
+  uint32_t _pad;
 } cagra_engine_opts;
 
 void cagra_engine_opts_default(cagra_engine_opts* o);

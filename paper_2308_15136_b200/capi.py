@@ -58,7 +58,8 @@ class SearchParamsC(C.Structure):
 class EngineOptsC(C.Structure):
     _fields_ = [("mode", C.c_uint32), ("team_count", C.c_uint32), ("num_threads", C.c_uint32),
                 ("seed_mode", C.c_uint32), ("query_offset", C.c_uint64),
-                ("exact_distances", C.c_uint32), ("team_size", C.c_uint32)]
+                ("exact_distances", C.c_uint32), ("team_size", C.c_uint32),
+                ("multi_cta", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 class SearchStatsC(C.Structure):

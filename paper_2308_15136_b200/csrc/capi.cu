@@ -216,8 +216,10 @@ struct cagra_index {
   size_t table_elems = 0;
   uint32_t table_hcap = 0, table_grid = 0;
   // per-call scratch
-  DBuf init_ids, work, q, ids, dists, counts, stats;
+  DBuf init_ids, work, q, ids, dists, counts, stats, team_out, team_stats;
   uint32_t last_launches = 0;
+  uint32_t mc_tag = 0;        // generation of the multi-CTA per-query tables
+  bool mc_layout = false;     // tables currently laid out per query
   ~cagra_index() { delete stream; }
 };
 
@@ -258,6 +260,7 @@ SearchConfig to_config(const cagra_search_params* p, const cagra_engine_opts* o)
   c.exact = o->exact_distances;
   c.team_size = o->team_size;
   c.query_offset = o->query_offset;
+  c.multi_cta = o->multi_cta;
   return c;
 }
 
@@ -274,8 +277,28 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
   SearchPlan pl = plan_search(v, c, nq, ix->sm_count, kTableBudget);
   ix->init_ids.ensure(sizeof(uint32_t) * std::max<size_t>(pl.init_elems, 1));
   ix->work.ensure(sizeof(uint32_t));
-  if (pl.table_elems) {
-    bool relayout = pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
+  if (pl.mc) {
+    ix->team_out.ensure(sizeof(unsigned long long) * std::max<size_t>(pl.team_elems, 1));
+    ix->team_stats.ensure(sizeof(cagra_search_stats) * (size_t)nq * pl.teams);
+    // per-query regions tagged by a call generation; a new layout starts clean
+    if (!ix->mc_layout || pl.hcap != ix->table_hcap || pl.table_elems > ix->table_elems ||
+        ix->mc_tag == 0xffffffffu) {
+      if (pl.table_elems > ix->table_elems) {
+        ix->tables.alloc(sizeof(unsigned long long) * pl.table_elems);
+        ix->table_elems = pl.table_elems;
+      }
+      CAGRA_CUDA_TRY(cudaMemsetAsync(ix->tables.p, 0, ix->tables.bytes, s));
+      ix->mc_tag = 0;
+      ix->table_hcap = pl.hcap;
+      ix->table_grid = 0;  // the per-CTA generations no longer match
+      ix->gens.ensure(sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
+      CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
+      ix->mc_layout = true;
+    }
+    ix->mc_tag++;
+    ix->gens.ensure(sizeof(uint32_t) * pl.grid);
+  } else if (pl.table_elems) {
+    bool relayout = ix->mc_layout || pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
                     pl.table_elems > ix->table_elems;
     if (relayout) {
       // a changed layout would alias old tags into other slots: start clean
@@ -288,6 +311,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
       ix->table_hcap = pl.hcap;
       ix->table_grid = std::max(pl.grid, ix->table_grid);
+      ix->mc_layout = false;
     }
   } else {
     ix->gens.ensure(sizeof(uint32_t) * pl.grid);
@@ -295,7 +319,8 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
   ix->last_launches = launch_search(v, c, pl, d_queries, nq, d_ids, d_dists, d_counts, d_stats,
                                     ix->init_ids.as<uint32_t>(), ix->work.as<uint32_t>(),
                                     ix->tables.as<unsigned long long>(), ix->gens.as<uint32_t>(),
-                                    s);
+                                    ix->team_out.as<unsigned long long>(), ix->team_stats.p,
+                                    ix->mc_tag, s);
 }
 
 }  // namespace
@@ -327,6 +352,8 @@ void cagra_search_params_default(cagra_search_params* p) {
 }
 
 void cagra_engine_opts_default(cagra_engine_opts* o) {
+  o->multi_cta = 0;
+  o->_pad = 0;
   o->mode = CAGRA_MODE_PER_QUERY;
   o->team_count = 4;
   o->num_threads = 0;

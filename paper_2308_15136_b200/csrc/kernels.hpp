@@ -76,6 +76,7 @@ struct SearchConfig {
   uint64_t seed;
   uint32_t mode, team_count, seed_mode, exact, team_size;
   uint64_t query_offset;
+  uint32_t multi_cta;  // 0 auto, 1 single-CTA lockstep teams, 2 one CTA per team
 };
 
 struct DeviceIndexView {
@@ -90,6 +91,8 @@ struct SearchPlan {
   size_t smem = 0;
   size_t table_elems = 0;  // u64 slots of HBM visited tables (grid * hcap)
   size_t init_elems = 0;   // u32 init sample ids
+  bool mc = false;         // shared mode with one CTA per (query, team)
+  size_t team_elems = 0;   // u64 team top-M keys (nq * teams * M) in mc mode
   const void* fn = nullptr;
 };
 // Validates device limits and picks the kernel variant / grid.
@@ -101,6 +104,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
                        const float* d_queries, uint32_t nq, uint32_t* d_ids, float* d_dists,
                        uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
                        uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
+                       unsigned long long* d_team_out, void* d_team_stats, uint32_t mc_tag,
                        cudaStream_t stream);
 
 // ---- merge.cu (K8) --------------------------------------------------------------

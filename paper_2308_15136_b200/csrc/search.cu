@@ -76,6 +76,11 @@ struct KParams {
   DevStats* stats;
   int* error;
   unsigned long long* prof;  // optional phase cycle counters (CAGRA_SEARCH_PROF)
+  // multi-CTA shared mode: work item qi = query * mc_teams + team; the teams
+  // of a query share the HBM visited region of the query (generation mc_tag)
+  uint32_t mc_teams, mc_tag;
+  unsigned long long* team_out;  // [nq * teams][M] team top-M keys
+  DevStats* team_stats;          // [nq * teams]
 };
 
 #define PROF_T(var) long long var = (P.prof && threadIdx.x == 0) ? clock64() : 0
@@ -214,6 +219,7 @@ __device__ __noinline__ void block_sort_any(uint64_t* a, uint32_t P) {
   else if (P == 512) block_sort_regs<2>(a);
   else if (P == 1024) block_sort_regs<4>(a);
   else if (P == 2048) block_sort_regs<8>(a);
+  else if (P == 4096) block_sort_regs<16>(a);
   else block_sort_smem(a, P);
 }
 
@@ -576,11 +582,17 @@ search_kernel(const KParams P) {
     const uint32_t qi = ctl.qi;
     if (qi >= P.nq) break;
     // ---- per-query setup
-    for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qi * P.ld + i];
+    const uint32_t qreal = P.mc_teams ? qi / P.mc_teams : qi;
+    for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qreal * P.ld + i];
     for (uint32_t i = tid; i < P.M; i += SNT) S.topA[i] = kDummyKey;
     if (SMEM_TABLE)
       for (uint32_t i = tid; i < P.hcap; i += SNT) S.table[i] = kInvalidId;
-    tag = tag + 1;
+    if (!SMEM_TABLE && P.mc_teams) {
+      gtab = P.gtables + (size_t)qreal * P.hcap;  // shared by the query's teams
+      tag = P.mc_tag;
+    } else {
+      tag = tag + 1;
+    }
     if (tid == 0) {
       ctl.nsurv[0] = 0;
       ctl.count = 0;
@@ -820,6 +832,21 @@ search_kernel(const KParams P) {
     if (pending) merge();
     DBG("q%u final merge\n", qi);
 
+    if (P.mc_teams) {
+      // multi-CTA: hand the team's whole top-M list to the team merge (K7)
+      for (uint32_t i = tid; i < P.M; i += SNT) P.team_out[(size_t)qi * P.M + i] = top[i];
+      if (tid == 0) {
+        DevStats st;
+        st.iterations = iters;
+        st.hash_resets = 0;
+        st.distance_evals = ctl.evals[0];
+        st.converged = converged ? 1u : 0u;
+        st.pad = 0;
+        P.team_stats[qi] = st;
+      }
+      __syncthreads();
+      continue;
+    }
     // ---- finish (search.cpp:247-259)
     uint32_t live;
     {
@@ -869,7 +896,83 @@ search_kernel(const KParams P) {
     }
     __syncthreads();
   }
-  if (!SMEM_TABLE && tid == 0) P.gens[blockIdx.x] = tag;
+  if (!SMEM_TABLE && !P.mc_teams && tid == 0) P.gens[blockIdx.x] = tag;
+}
+
+// ------------------------------------------------------ K7 team merge ------
+// merge_team_results (engine.cpp:12-36) for the multi-CTA shared mode: per
+// query the union of the T team top-M lists sorted by (dist, id), ids
+// deduplicated, first k; re-scored with the sequential chain in fast mode.
+// Stats: evaluations summed, iterations max, converged = all teams.
+__global__ void __launch_bounds__(SNT)
+team_merge_kernel(const unsigned long long* __restrict__ team_out,
+                  const DevStats* __restrict__ team_stats, uint32_t T, uint32_t M, uint32_t k,
+                  const float* __restrict__ data, uint32_t ld, uint32_t dim,
+                  const float* __restrict__ queries, uint32_t exact, uint32_t* __restrict__ out_ids,
+                  float* __restrict__ out_dists, uint32_t* __restrict__ out_counts,
+                  DevStats* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t total = T * M, P2 = max(256u, next_pow2_u32(total));
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);   // P2
+  uint64_t* fin = keys + P2;                                  // 256
+  __shared__ uint32_t nfin;
+  for (uint32_t i = tid; i < P2; i += SNT)
+    keys[i] = i < total ? cmp_key(team_out[(size_t)q * total + i]) : kDummyKey;
+  __syncthreads();
+  block_sort_any(keys, P2);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t w = 0, prev = kInvalidId;
+    for (uint32_t i = 0; i < P2 && w < k; ++i) {
+      const uint64_t e = keys[i];
+      if (key_is_dummy(e)) break;
+      if (key_id(e) == prev) continue;
+      prev = key_id(e);
+      fin[w++] = e;
+    }
+    nfin = w;
+  }
+  __syncthreads();
+  const uint32_t live = nfin;
+  if (!exact) {
+    const float* qv = queries + (size_t)q * ld;
+    for (uint32_t i = tid; i < live; i += SNT) {
+      const uint32_t id = key_id(fin[i]);
+      const float* x = data + (size_t)id * ld;
+      float acc = 0.0f;
+      for (uint32_t d = 0; d < dim; ++d) acc = seq_step(acc, __ldg(x + d), __ldg(qv + d));
+      fin[i] = make_key(acc, id);
+    }
+    __syncthreads();
+    if (warp == 0) warp_sort_smem(fin, live, lane);
+    __syncthreads();
+  }
+  for (uint32_t i = tid; i < k; i += SNT) {
+    const bool ok = i < live;
+    out_ids[(size_t)q * k + i] = ok ? key_id(fin[i]) : kInvalidId;
+    out_dists[(size_t)q * k + i] = ok ? key_dist(fin[i]) : __int_as_float(0x7f800000);
+  }
+  if (tid == 0) {
+    out_counts[q] = live;
+    if (stats) {
+      DevStats st;
+      unsigned long long ev = 0;
+      uint32_t it = 0, cv = 1;
+      for (uint32_t t = 0; t < T; ++t) {
+        const DevStats& s = team_stats[(size_t)q * T + t];
+        ev += s.distance_evals;
+        it = max(it, s.iterations);
+        cv = cv && s.converged;
+      }
+      st.iterations = it;
+      st.hash_resets = 0;
+      st.distance_evals = ev;
+      st.converged = cv;
+      st.pad = 0;
+      stats[q] = st;
+    }
+  }
 }
 
 
@@ -1208,25 +1311,32 @@ KernelFn shared_fn(bool exact, Variant v) {
 SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_t nq,
                        int sm_count, size_t table_budget) {
   SearchPlan pl;
-  const bool shared = c.mode == 1;
-  const uint32_t T = shared ? c.team_count : 1;
+  const bool shared_mode = c.mode == 1;
+  // multi-CTA shared mode: one CTA per (query, team), racing on a shared
+  // visited table (reference order is kept only by the lockstep kernel)
+  pl.mc = shared_mode && !c.exact && c.multi_cta != 1 &&
+          (c.multi_cta == 2 || nq < (uint32_t)sm_count);
+  const bool shared = shared_mode && !pl.mc;  // single-CTA lockstep teams
+  const uint32_t T = shared_mode ? c.team_count : 1;
   if (shared && (T < 2 || T > 16))
-    throw UsageErr("batch_search: shared mode supports 2 <= team_count <= 16 on device");
-  const uint32_t p = shared ? 1 : c.width;
+    throw UsageErr("batch_search: lockstep shared mode supports 2 <= team_count <= 16");
+  if (pl.mc && (T < 2 || T > 256))
+    throw UsageErr("batch_search: multi-CTA shared mode supports 2 <= team_count <= 256");
+  const uint32_t p = shared_mode ? 1 : c.width;
   const uint32_t d = ix.degree;
   const uint32_t C = p * d;
   const uint32_t imax = resolved_max_iter(c.max_iter, c.topm, p);
   pl.teams = T;
   pl.C = C;
   pl.max_iter = imax;
-  pl.min_iter = shared ? std::min(c.min_iter, imax) : c.min_iter;  // engine.cpp:45
-  const bool forget = !shared && c.hash_policy == 1;
+  pl.min_iter = shared_mode ? std::min(c.min_iter, imax) : c.min_iter;  // engine.cpp:45
+  const bool forget = !shared_mode && c.hash_policy == 1;
   uint64_t hcap;
   if (forget) {
     hcap = 1ull << c.hash_bits;
   } else {
     // VisitedTable::standard_sized (search.cpp:104-108)
-    uint64_t expected = (uint64_t)(imax + 1) * (shared ? T : p) * d;
+    uint64_t expected = (uint64_t)(imax + 1) * (shared_mode ? T : p) * d;
     uint64_t want = 2 * std::max<uint64_t>(1, expected), cap = 1;
     while (cap < want) cap <<= 1;
     if (cap > (1ull << 31)) throw UsageErr("visited table capacity overflow");
@@ -1261,8 +1371,15 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   CAGRA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SNT, smem));
   if (occ < 1) throw UsageErr("search: kernel cannot be resident with these parameters");
   uint64_t grid = (uint64_t)sm_count * occ;
-  if (grid > nq) grid = nq ? nq : 1;
-  if (!pl.smem_table) {
+  const uint64_t items = pl.mc ? (uint64_t)nq * T : nq;
+  if (grid > items) grid = items ? items : 1;
+  if (pl.mc) {
+    // one visited region per query, shared by its teams
+    if ((uint64_t)nq * hcap * 8 > table_budget)
+      throw UsageErr("search: multi-CTA visited tables exceed the device memory budget");
+    pl.table_elems = (uint64_t)nq * hcap;
+    pl.team_elems = (uint64_t)nq * T * c.topm;
+  } else if (!pl.smem_table) {
     uint64_t per = hcap * 8;
     uint64_t maxg = table_budget / per;
     if (maxg < 1) throw UsageErr("search: visited table exceeds the device memory budget");
@@ -1280,6 +1397,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
                        const float* d_queries, uint32_t nq, uint32_t* d_ids, float* d_dists,
                        uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
                        uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
+                       unsigned long long* d_team_out, void* d_team_stats, uint32_t mc_tag,
                        cudaStream_t stream) {
   if (nq == 0) return 0;
   dim3 ig((nq + 127) / 128, pl.teams);
@@ -1297,17 +1415,21 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.degree = ix.degree;
   P.deg_shift = (ix.degree & (ix.degree - 1)) == 0 ? (uint32_t)__builtin_ctz(ix.degree) : 0xffu;
   P.queries = d_queries;
-  P.nq = nq;
+  P.nq = pl.mc ? nq * pl.teams : nq;
   P.k = c.k;
   P.M = c.topm;
-  P.p = pl.teams > 1 ? 1 : c.width;
+  P.p = c.mode == 1 ? 1 : c.width;
   P.C = pl.C;
   P.max_iter = pl.max_iter;
   P.min_iter = pl.min_iter;
-  P.policy = pl.teams > 1 ? 0 : c.hash_policy;
+  P.policy = c.mode == 1 ? 0 : c.hash_policy;
   P.reset_interval = c.reset_interval ? c.reset_interval : 1;
   P.hcap = pl.hcap;
-  P.teams = pl.teams;
+  P.teams = pl.mc ? 1 : pl.teams;
+  P.mc_teams = pl.mc ? pl.teams : 0;
+  P.mc_tag = mc_tag;
+  P.team_out = d_team_out;
+  P.team_stats = reinterpret_cast<DevStats*>(d_team_stats);
   P.init_ids = d_init_ids;
   P.gtables = d_tables;
   P.gens = d_gens;
@@ -1328,6 +1450,20 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(pl.fn));
   fn<<<pl.grid, SNT, pl.smem, stream>>>(P);
   CAGRA_LAUNCH_CHECK();
+  uint32_t launches = 2;
+  if (pl.mc) {
+    const uint32_t total = pl.teams * c.topm;
+    const uint32_t P2 = std::max(256u, next_pow2_u32(total));
+    const size_t msmem = 8ull * (P2 + 256);
+    CAGRA_CUDA_TRY(cudaFuncSetAttribute(team_merge_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+    team_merge_kernel<<<nq, SNT, msmem, stream>>>(
+        d_team_out, reinterpret_cast<const DevStats*>(d_team_stats), pl.teams, c.topm, c.k,
+        ix.data, ix.ld, ix.dim, d_queries, c.exact, d_ids, d_dists, d_counts,
+        reinterpret_cast<DevStats*>(d_stats));
+    CAGRA_LAUNCH_CHECK();
+    launches = 3;
+  }
   if (P.prof) {
     unsigned long long h[8];
     CAGRA_CUDA_TRY(cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -1339,7 +1475,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
             100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot,
             100 * h[4] / tot);
   }
-  return 2;
+  return launches;
 }
 
 }  // namespace cagra

@@ -111,10 +111,12 @@ class EngineOptions:
     device: int = 0
     exact_distances: bool = False
     team_size: int = 0
+    multi_cta: int = 0  # shared mode: 0 auto, 1 lockstep single CTA, 2 one CTA per team
 
     def c(self, seed_mode=0, query_offset=0) -> capi.EngineOptsC:
         return capi.EngineOptsC(int(self.mode), self.team_count, self.num_threads, seed_mode,
-                                query_offset, int(bool(self.exact_distances)), self.team_size)
+                                query_offset, int(bool(self.exact_distances)), self.team_size,
+                                self.multi_cta, 0)
 
 
 @dataclass

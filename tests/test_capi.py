@@ -51,7 +51,7 @@ def test_host_helpers():
 
 def test_struct_layouts_match_header():
     assert C.sizeof(capi.SearchParamsC) == 40
-    assert C.sizeof(capi.EngineOptsC) == 32
+    assert C.sizeof(capi.EngineOptsC) == 40
     assert C.sizeof(capi.SearchStatsC) == 24 == capi.STATS_DTYPE.itemsize
     p = C.create_string_buffer(40)
     capi.lib().cagra_search_params_default(p)

@@ -232,8 +232,9 @@ def _golden_search(gpu, oracle, name, exact):
     for gi, (mode, m, p, pol, hb, ri, teams, seed) in enumerate(g["grid"].tolist()):
         prm = fodg.SearchParams(k=10, topm=m, width=p, hash_policy=fodg.HashPolicy(pol),
                                 hash_bits=hb, reset_interval=ri, seed=seed)
+        # multi_cta=1: the lockstep team order (multi-CTA has its own test)
         opts = fodg.EngineOptions(mode=fodg.ExecutionMode(mode), team_count=teams,
-                                  exact_distances=exact)
+                                  exact_distances=exact, multi_cta=1)
         ids, dists, counts, st = ix.search(queries, prm, opts)
         out.append((gi, g, ids, dists, counts, st))
     return out
@@ -273,6 +274,43 @@ def test_search_fast_mode_parity(gpu, oracle, name):
             if ids[q, j] == capi.INVALID_ID:
                 continue
             assert bits(dists[q, j]) == bits(fodg.squared_l2(data[ids[q, j]], queries[q]))
+
+
+@pytest.mark.parametrize("name", CORPORA)
+def test_multi_cta_shared_mode_parity(gpu, oracle, name):
+    """Shared mode with one CTA per team (teams race on one visited table):
+    recall within 0.5 pp of the reference's lockstep shared mode
+    (engine.cpp:38-78) at the same params and seeds; reported distances are
+    the sequential chain; evaluations >= the per-query p=1 run."""
+    g, data, queries = corpus(oracle, name)
+    ds = fodg.Dataset.from_array(data)
+    ix = fodg.Index(ds, fodg.Graph(int(g["n"]), int(g["d"]), g["graph"]))
+    gt = g["gt_ids"]
+    for m, teams in [(32, 4), (64, 8)]:
+        prm = fodg.SearchParams(k=10, topm=m, width=1, seed=11)
+        ids, dists, counts, st = ix.search(
+            queries, prm, fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers,
+                                             team_count=teams, multi_cta=2))
+        assert ix.last_launch_count() == 3
+        o = oracle.batch_search(g["graph"], data, queries, make_params(k=10, topm=m, width=1,
+                                                                       seed=11),
+                                mode=1, team_count=teams)
+        nq = gt.shape[0]
+        rec = np.mean([len(set(ids[q]) & set(gt[q])) / 10 for q in range(nq)])
+        ref_rec = np.mean([len(set(o[0][q]) & set(gt[q])) / 10 for q in range(nq)])
+        assert abs(rec - ref_rec) <= 0.005, (m, teams, rec, ref_rec)
+        assert np.mean(ids == o[0]) >= 0.95
+        assert (counts == 10).all()
+        for q in range(0, nq, 23):
+            for j in range(10):
+                assert bits(dists[q, j]) == bits(fodg.squared_l2(data[ids[q, j]], queries[q]))
+        # lockstep (reference order) still available and bit-exact in exact mode
+        ids2, dists2, _, st2 = ix.search(
+            queries, prm, fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers,
+                                             team_count=teams, multi_cta=1,
+                                             exact_distances=True))
+        assert np.array_equal(ids2, o[0])
+        assert np.array_equal(st2["distance_evals"], o[3]["distance_evals"])
 
 
 def test_batch_equals_search_one(gpu, oracle):
