@@ -153,19 +153,29 @@ int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* rera
 int cagra_count_detourable_routes(const uint32_t* knn_ids, const float* knn_dists,
                                   uint32_t n, uint32_t deg, int device,
                                   uint32_t* counts_out);
+/* count_detourable_routes (graph_opt.hpp:47-49), distance mode — the paper's
+ * comparison variant: every leg recomputed from the vectors (graph_opt.cpp:
+ * 66-71, 87-93).  data: ds_n x dim host rows (NULL -> USAGE, as the
+ * reference's "distance mode requires the dataset"). */
+int cagra_count_detourable_routes_distance(const uint32_t* knn_ids, const float* knn_dists,
+                                           uint32_t n, uint32_t deg, const float* data,
+                                           uint32_t ds_n, uint32_t dim, int device,
+                                           uint32_t* counts_out);
 /* reorder_and_prune (graph_opt.hpp:53-54). */
 int cagra_reorder_and_prune(const uint32_t* knn_ids, const uint32_t* counts, uint32_t n,
                             uint32_t deg, uint32_t d, int device, uint32_t* pruned_out);
-/* build_reverse_graph (graph_opt.hpp:59): rev rows in CSR form; row y holds at
- * most `cap` sources ordered by (rank, source).  rev_counts_out[n],
- * rev_ids_out[n*cap] (row y at y*cap, first rev_counts_out[y] valid). */
+/* build_reverse_graph (graph_opt.hpp:59): row y holds at most `cap` sources
+ * ordered by (rank, source).  With c = min(cap, n) (a cap above n means no
+ * cap): rev_counts_out[n], rev_ids_out[n*c] (row y at y*c, first
+ * rev_counts_out[y] valid). */
 int cagra_build_reverse_graph(const uint32_t* pruned, uint32_t n, uint32_t d, uint32_t cap,
                               int device, uint32_t* rev_counts_out, uint32_t* rev_ids_out);
 /* merge_graphs (graph_opt.hpp:63) on the CSR reverse form above. */
 int cagra_merge_graphs(const uint32_t* pruned, const uint32_t* rev_counts,
                        const uint32_t* rev_ids, uint32_t n, uint32_t d, uint32_t rev_cap,
                        int device, uint32_t* graph_out);
-/* optimize (graph_opt.hpp:67-68) with OptimizeOptions{kRank, reorder, add_reverse}. */
+/* optimize (graph_opt.hpp:67-68) with OptimizeOptions{kRank, reorder, add_reverse}.
+ * knn_dists may be NULL when reorder = 0 (plain truncation). */
 int cagra_optimize(const uint32_t* knn_ids, const float* knn_dists, uint32_t n,
                    uint32_t deg, uint32_t d, uint32_t reorder, uint32_t add_reverse,
                    int device, uint32_t* graph_out, cagra_opt_stats* stats);

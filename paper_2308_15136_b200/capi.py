@@ -83,7 +83,7 @@ EXPORTS = [
     "cagra_last_error", "cagra_version", "cagra_device_count", "cagra_search_params_default",
     "cagra_engine_opts_default", "cagra_uniform_dataset", "cagra_mix_seed",
     "cagra_exact_knn_graph", "cagra_exact_topk", "cagra_knn_last_stats",
-    "cagra_count_detourable_routes",
+    "cagra_count_detourable_routes", "cagra_count_detourable_routes_distance",
     "cagra_reorder_and_prune", "cagra_build_reverse_graph", "cagra_merge_graphs",
     "cagra_optimize", "cagra_build_graph", "cagra_index_create", "cagra_index_create_dev",
     "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
@@ -112,6 +112,8 @@ def lib() -> C.CDLL:
         L.cagra_exact_topk.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp]
         L.cagra_knn_last_stats.argtypes = [vp, vp, vp, vp]
         L.cagra_count_detourable_routes.argtypes = [vp, vp, u32, u32, i32, vp]
+        L.cagra_count_detourable_routes_distance.argtypes = [vp, vp, u32, u32, vp, u32, u32, i32,
+                                                             vp]
         L.cagra_reorder_and_prune.argtypes = [vp, vp, u32, u32, u32, i32, vp]
         L.cagra_build_reverse_graph.argtypes = [vp, u32, u32, u32, i32, vp, vp]
         L.cagra_merge_graphs.argtypes = [vp, vp, vp, u32, u32, u32, i32, vp]

@@ -155,7 +155,9 @@ void optimize_device(const uint32_t* d_knn, const float* d_dists, uint32_t n, ui
   int hflag = 0;
   CAGRA_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
   launch_check_ids(d_knn, (uint64_t)n * deg, n, flag.as<int>(), s);
-  launch_check_sorted(d_knn, d_dists, n, deg, flag.as<int>(), s);
+  // rank-mode reordering requires distance-sorted rows (graph_opt.cpp:19-31);
+  // plain truncation (reorder = false) does not read distances
+  if (reorder) launch_check_sorted(d_knn, d_dists, n, deg, flag.as<int>(), s);
   read_flag(flag.as<int>(), &hflag, s);
   if (hflag & 2) throw UsageErr("optimize: neighbour id out of range");
   if (hflag & 1) throw UsageErr("graph_opt: input rows must be distance-sorted");
@@ -454,6 +456,41 @@ int cagra_count_detourable_routes(const uint32_t* knn_ids, const float* knn_dist
   });
 }
 
+int cagra_count_detourable_routes_distance(const uint32_t* knn_ids, const float* knn_dists,
+                                           uint32_t n, uint32_t deg, const float* data,
+                                           uint32_t ds_n, uint32_t dim, int device,
+                                           uint32_t* counts_out) {
+  return guarded([&] {
+    if (n == 0 || deg == 0) return;
+    // graph_opt.cpp:45-51: sortedness first, then the dataset checks
+    if (!knn_dists) throw UsageErr("graph_opt: input rows have no distances");
+    int dev = resolve_device(device);
+    DeviceScope scope(dev);
+    Stream st;
+    size_t e = (size_t)n * deg;
+    DBuf di(4 * e), dd(4 * e), dc(4 * e), flag(sizeof(int));
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(di.p, knn_ids, 4 * e, cudaMemcpyHostToDevice, st.s));
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(dd.p, knn_dists, 4 * e, cudaMemcpyHostToDevice, st.s));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st.s));
+    launch_check_sorted(di.as<uint32_t>(), dd.as<float>(), n, deg, flag.as<int>(), st.s);
+    launch_check_ids(di.as<uint32_t>(), e, n, flag.as<int>(), st.s);
+    int h = 0;
+    read_flag(flag.as<int>(), &h, st.s);
+    if (h & 1) throw UsageErr("graph_opt: input rows must be distance-sorted");
+    if (!data) throw UsageErr("count_detourable_routes: distance mode requires the dataset");
+    if (ds_n != n) throw UsageErr("count_detourable_routes: dataset/graph size mismatch");
+    if (h & 2) throw UsageErr("graph_opt: neighbour id out of range");
+    if (dim == 0) throw UsageErr("dataset dimension must be >= 1");
+    const uint32_t ld = row_stride(dim);
+    DBuf dx(sizeof(float) * (size_t)n * ld);
+    upload_rows(dx.as<float>(), data, n, dim, ld, st.s);
+    launch_detour_distance(di.as<uint32_t>(), n, deg, dx.as<float>(), ld, dim, dc.as<uint32_t>(),
+                           st.s);
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(counts_out, dc.p, 4 * e, cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+  });
+}
+
 int cagra_reorder_and_prune(const uint32_t* knn_ids, const uint32_t* counts, uint32_t n,
                             uint32_t deg, uint32_t d, int device, uint32_t* pruned_out) {
   return guarded([&] {
@@ -481,6 +518,7 @@ int cagra_build_reverse_graph(const uint32_t* pruned, uint32_t n, uint32_t d, ui
     DeviceScope scope(dev);
     Stream st;
     size_t e = (size_t)n * d;
+    cap = std::min(cap, n);  // no row holds more than n sources: larger caps mean "no cap"
     DBuf dp(4 * e), flag(sizeof(int)), sc(reverse_scratch_bytes(n, d)), rc(4ull * n),
         ri(4ull * n * std::max(cap, 1u));
     CAGRA_CUDA_TRY(cudaMemcpyAsync(dp.p, pruned, 4 * e, cudaMemcpyHostToDevice, st.s));
@@ -539,8 +577,10 @@ int cagra_optimize(const uint32_t* knn_ids, const float* knn_dists, uint32_t n, 
     Stream st;
     size_t e = (size_t)n * deg;
     DBuf di(4 * e), dd(4 * e), out(4ull * n * d);
+    if (reorder && !knn_dists) throw UsageErr("graph_opt: input rows have no distances");
     CAGRA_CUDA_TRY(cudaMemcpyAsync(di.p, knn_ids, 4 * e, cudaMemcpyHostToDevice, st.s));
-    CAGRA_CUDA_TRY(cudaMemcpyAsync(dd.p, knn_dists, 4 * e, cudaMemcpyHostToDevice, st.s));
+    if (knn_dists)
+      CAGRA_CUDA_TRY(cudaMemcpyAsync(dd.p, knn_dists, 4 * e, cudaMemcpyHostToDevice, st.s));
     OptOut t;
     optimize_device(di.as<uint32_t>(), dd.as<float>(), n, deg, d, reorder != 0, add_reverse != 0,
                     out.as<uint32_t>(), st.s, &t);

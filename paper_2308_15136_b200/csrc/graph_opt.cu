@@ -7,6 +7,8 @@
 // Integer work only; every output position is a pure function of the input
 // rows (atomics only accumulate counts or claim bucket slots that are sorted
 // afterwards), so results never depend on scheduling.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -140,6 +142,78 @@ detour_reorder_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t deg
   }
 }
 
+// Distance-mode detour counting (graph_opt.cpp:66-71, 87-93), the paper's
+// comparison variant: every leg is recomputed from the vectors with the
+// sequential fp32 chain (w(X->Z), w(Z->Y), w(X->Y)); a route counts when
+// max(w(X->Z), w(Z->Y)) < w(X->Y).  One CTA per node X.
+// Shared layout: xrow[deg] | hkey[H] | hrank[H] | counts[deg] | xdist[deg]
+__global__ void __launch_bounds__(OPT_NT)
+detour_distance_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t deg, uint32_t H,
+                       const float* __restrict__ data, uint32_t ld, uint32_t dim,
+                       uint32_t* __restrict__ counts_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* xrow = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* hkey = xrow + deg;
+  uint32_t* hrank = hkey + H;
+  uint32_t* counts = hrank + H;
+  float* xdist = reinterpret_cast<float*>(counts + deg);
+  const uint32_t hmask = H - 1;
+  auto dist = [&](uint32_t a, uint32_t b) {
+    const float* pa = data + (size_t)a * ld;
+    const float* pb = data + (size_t)b * ld;
+    float acc = 0.0f;
+    for (uint32_t i = 0; i < dim; ++i) acc = seq_step(acc, __ldg(pa + i), __ldg(pb + i));
+    return acc;
+  };
+  for (uint32_t x = blockIdx.x; x < n; x += gridDim.x) {
+    const uint32_t* xr = knn + (size_t)x * deg;
+    for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) {
+      hkey[i] = kInvalidId;
+      hrank[i] = kInvalidId;
+    }
+    for (uint32_t r = threadIdx.x; r < deg; r += blockDim.x) {
+      xrow[r] = xr[r];
+      counts[r] = 0;
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < deg; r += blockDim.x) {
+      const uint32_t id = xrow[r];
+      uint32_t h = hash_id(id, hmask);
+      for (;;) {
+        uint32_t old = atomicCAS(&hkey[h], kInvalidId, id);
+        if (old == kInvalidId || old == id) break;
+        h = (h + 1) & hmask;
+      }
+      atomicMin(&hrank[h], r);
+      xdist[r] = dist(x, id);
+    }
+    __syncthreads();
+    for (uint32_t pi = threadIdx.x; pi < deg * deg; pi += blockDim.x) {
+      const uint32_t rz = pi / deg, rzy = pi - rz * deg;
+      const uint32_t z = xrow[rz];
+      const uint32_t y = __ldg(&knn[(size_t)z * deg + rzy]);
+      if (y == x) continue;
+      uint32_t h = hash_id(y, hmask), ry = kInvalidId;
+      for (;;) {
+        const uint32_t k = hkey[h];
+        if (k == y) {
+          ry = hrank[h];
+          break;
+        }
+        if (k == kInvalidId) break;
+        h = (h + 1) & hmask;
+      }
+      if (ry == kInvalidId || ry == rz) continue;
+      const float wzy = dist(z, y);
+      const float a = xdist[rz];
+      if ((a < wzy ? wzy : a) < xdist[ry]) atomicAdd(&counts[ry], 1u);
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < deg; r += blockDim.x) counts_out[(size_t)x * deg + r] = counts[r];
+    __syncthreads();
+  }
+}
+
 size_t detour_smem(uint32_t deg, uint32_t H, uint32_t P) {
   return sizeof(uint64_t) * P + sizeof(uint32_t) * (deg + 2 * H + deg);
 }
@@ -256,10 +330,13 @@ reverse_select_kernel(const unsigned long long* __restrict__ start,
                       uint32_t* __restrict__ rev_counts, uint32_t* __restrict__ rev_ids) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + warp * REV_BUF;
+  // per-warp key buffer: the best `cap` so far + the next chunk of in-edges
   const uint32_t capP = next_pow2_u32(cap);
-  const uint32_t chunk = REV_BUF - capP;
-  for (uint32_t y = blockIdx.x * REV_WARPS + warp; y < n; y += gridDim.x * REV_WARPS) {
+  const uint32_t rev_buf = capP <= REV_BUF / 2 ? REV_BUF : 2 * capP;
+  const uint32_t nwarps = blockDim.x >> 5;
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * rev_buf;
+  const uint32_t chunk = rev_buf - capP;
+  for (uint32_t y = blockIdx.x * nwarps + warp; y < n; y += gridDim.x * nwarps) {
     unsigned long long b = start[y], e = start[y + 1];
     uint32_t len = (uint32_t)(e - b);
     uint32_t have = 0;  // sorted best prefix in buf[0..have)
@@ -396,6 +473,20 @@ void launch_detour_reorder(const uint32_t* d_knn, uint32_t n, uint32_t deg, uint
   detour_launch(d_knn, nullptr, n, deg, d, d_counts_out, d_pruned_out, stream);
 }
 
+void launch_detour_distance(const uint32_t* d_knn, uint32_t n, uint32_t deg, const float* d_data,
+                            uint32_t ld, uint32_t dim, uint32_t* d_counts_out,
+                            cudaStream_t stream) {
+  const uint32_t H = next_pow2_u32(2 * deg);
+  const size_t smem = sizeof(uint32_t) * (2 * (size_t)deg + 2 * H) + sizeof(float) * deg;
+  if (smem > 200 * 1024) throw UsageErr("optimize: input degree too large for the device kernel");
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(detour_distance_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)(n < 148u * 64u ? n : 148u * 64u);
+  detour_distance_kernel<<<grid, OPT_NT, smem, stream>>>(d_knn, n, deg, H, d_data, ld, dim,
+                                                         d_counts_out);
+  CAGRA_LAUNCH_CHECK();
+}
+
 void launch_reorder_from_counts(const uint32_t* d_knn, const uint32_t* d_counts, uint32_t n,
                                 uint32_t deg, uint32_t d, uint32_t* d_pruned_out,
                                 cudaStream_t stream) {
@@ -418,7 +509,10 @@ static char* carve(char*& p, size_t bytes) {
 void launch_reverse(const uint32_t* d_pruned, uint32_t n, uint32_t d, uint32_t cap,
                     void* d_scratch, uint32_t* d_rev_counts, uint32_t* d_rev_ids,
                     cudaStream_t stream) {
-  if (cap > 512) throw UsageErr("build_reverse_graph: cap > 512 unsupported on device");
+  // rows never hold more than their in-degree: a cap above the largest
+  // possible in-degree (n) is "no cap" (graph_opt.cpp:141-160)
+  if (cap > n) cap = n;
+  if (cap > 8192) throw UsageErr("build_reverse_graph: cap > 8192 unsupported on device");
   char* p = reinterpret_cast<char*>(d_scratch);
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) / 256 * 256);
   uint32_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -443,11 +537,14 @@ void launch_reverse(const uint32_t* d_pruned, uint32_t n, uint32_t d, uint32_t c
   reverse_scatter_kernel<<<grid_for(edges, 256), 256, 0, stream>>>(d_pruned, n, d, start, fill,
                                                                    keys);
   CAGRA_LAUNCH_CHECK();
-  size_t smem = sizeof(uint64_t) * REV_BUF * REV_WARPS;
+  const uint32_t capP = next_pow2_u32(cap);
+  const uint32_t rev_buf = capP <= REV_BUF / 2 ? REV_BUF : 2 * capP;
+  const uint32_t warps = std::max<uint32_t>(1, std::min<uint32_t>(REV_WARPS, (96u << 10) / (8u * rev_buf)));
+  size_t smem = sizeof(uint64_t) * rev_buf * warps;
   CAGRA_CUDA_TRY(cudaFuncSetAttribute(reverse_select_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int grid = (int)std::min<uint64_t>((n + REV_WARPS - 1) / REV_WARPS, 148ull * 16);
-  reverse_select_kernel<<<grid, REV_WARPS * 32, smem, stream>>>(start, keys, n, cap,
+  int grid = (int)std::min<uint64_t>((n + warps - 1) / warps, 148ull * 16);
+  reverse_select_kernel<<<grid, warps * 32, smem, stream>>>(start, keys, n, cap,
                                                                 d_rev_counts, d_rev_ids);
   CAGRA_LAUNCH_CHECK();
 }

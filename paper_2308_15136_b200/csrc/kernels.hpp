@@ -49,6 +49,10 @@ void launch_check_ids(const uint32_t* d_ids, uint64_t count, uint32_t n, int* d_
 void launch_detour_reorder(const uint32_t* d_knn, uint32_t n, uint32_t deg, uint32_t d,
                            uint32_t* d_counts_out, uint32_t* d_pruned_out,
                            cudaStream_t stream);
+// distance-mode detour counts (graph_opt.cpp:66-71, 87-93); data rows of ld floats.
+void launch_detour_distance(const uint32_t* d_knn, uint32_t n, uint32_t deg, const float* d_data,
+                            uint32_t ld, uint32_t dim, uint32_t* d_counts_out,
+                            cudaStream_t stream);
 // reorder only, from given counts (reorder_and_prune)
 void launch_reorder_from_counts(const uint32_t* d_knn, const uint32_t* d_counts, uint32_t n,
                                 uint32_t deg, uint32_t d, uint32_t* d_pruned_out,

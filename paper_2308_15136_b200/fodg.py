@@ -384,7 +384,7 @@ def truncate_graph(g: KnnGraph, d: int) -> Graph:
 def _reverse_arrays(pruned: Graph, cap: int, device: int = 0):
     ids = np.ascontiguousarray(pruned.ids, np.uint32)
     rc = np.empty(pruned.num_nodes, np.uint32)
-    ri = np.empty((pruned.num_nodes, max(cap, 1)), np.uint32)
+    ri = np.empty((pruned.num_nodes, max(min(cap, pruned.num_nodes), 1)), np.uint32)
     check(lib().cagra_build_reverse_graph(ptr(ids), pruned.num_nodes, pruned.degree, cap,
                                           device, ptr(rc), ptr(ri)))
     return rc, ri

@@ -1,0 +1,36 @@
+// Bridge from the fodg:: drop-in to the C ABI (include/cagra/capi.h):
+// status codes -> the reference's exception types, device selection, and the
+// cache of device-resident indexes that stands in for the reference's
+// per-call `const Graph&, const Dataset&` (re-uploading the index on every
+// batch_search would dominate).
+#pragma once
+
+#include <cstdint>
+
+#include "cagra/capi.h"
+#include "fodg/dataset.hpp"
+#include "fodg/graph.hpp"
+
+namespace fodg::b200 {
+
+/// Throws UsageError / FormatError / std::logic_error / std::runtime_error
+/// for a non-zero cagra status (message from cagra_last_error()).
+void check(int rc);
+
+/// CUDA device used by the drop-in (env CAGRA_DEVICE, default 0).
+int device();
+
+/// Fast in-loop distances (team reductions; reported distances still the
+/// sequential chain) instead of the reference-order chain everywhere.  Off by
+/// default so the drop-in reproduces the reference bit for bit; env
+/// CAGRA_FAST_DISTANCES=1 turns it on.
+bool fast_distances();
+
+/// The device index for (graph, ds), created on first use and reused while
+/// the host buffers are unchanged.
+cagra_index* index_for(const Graph& graph, const Dataset& ds);
+
+/// SM count of device() (the default b_T of choose_mode).
+unsigned device_sm_count();
+
+}  // namespace fodg::b200

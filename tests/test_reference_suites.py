@@ -1,0 +1,61 @@
+"""The reference's OWN unit suites and acceptance binary, compiled unchanged
+from /root/reference/proj/tests against the C++ drop-in (include/fodg +
+libfodg_b200.so -> libcagra_b200.so), run on the B200.
+
+The binaries are built here by `make refsuite` (tests/compat/doctest.h stands
+in for the absent vendor/doctest) and travel to the GPU box as build
+artefacts; nothing here reads /root/reference at run time.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITE_DIR = os.path.join(ROOT, "tests", "_refsuite")
+SUITES = ["test_core", "test_knn_build", "test_graph_opt", "test_search", "test_engine",
+          "test_io", "test_graph_metrics"]
+HOST_ONLY = ["test_io"]  # file formats: no device call
+
+
+def _bin(name):
+    path = os.path.join(SUITE_DIR, name)
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run `make refsuite` where /root/reference exists")
+    return path
+
+
+def _run(path, *args, timeout=1200):
+    return subprocess.run([path, *args], capture_output=True, text=True, timeout=timeout,
+                          cwd="/tmp")
+
+
+@pytest.mark.parametrize("suite", HOST_ONLY)
+def test_reference_host_suite(suite):
+    r = _run(_bin(suite))
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", [s for s in SUITES if s not in HOST_ONLY])
+def test_reference_unit_suite_on_b200(gpu, suite):
+    r = _run(_bin(suite))
+    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest-compat]")]
+    assert summary, r.stdout + r.stderr
+    assert r.returncode == 0, summary[0] + "\n" + r.stderr[-4000:]
+    m = re.search(r"(\d+) failed \| checks: (\d+) \| (\d+) failed", summary[0])
+    assert m and int(m.group(1)) == 0 and int(m.group(3)) == 0, summary[0]
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_on_b200(gpu):
+    cli = os.path.join(ROOT, "paper_2308_15136_b200", "lib", "fodg")
+    args = [cli] if os.path.exists(cli) else []
+    r = _run(_bin("acceptance"), *args)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("criterion ")]
+    assert len(lines) == 10, r.stdout + r.stderr
+    for line in lines[:9]:
+        assert ": PASS" in line, "\n".join(lines)
+    if args:
+        assert ": PASS" in lines[9], lines[9]
