@@ -1,0 +1,114 @@
+"""Multi-GPU search on one box: one process per GPU (torch.distributed).
+
+Two layouts; the reference itself has no distributed code:
+
+* query-sharded (replicated index) — every rank holds the whole index and
+  searches its own contiguous slice of the batch; no collective on the data
+  path.  `query_slice` gives the slice and the `query_offset` that keeps every
+  query's seed (mix_seed(seed ^ (0x0bad + global index)), engine.cpp:108)
+  identical to a single-GPU run, so results do not depend on the GPU count.
+
+* dataset-sharded — rank r indexes the contiguous id range `shard_bounds(n,
+  G)[r]` with its own graph (ids local to the shard); every rank searches
+  every query, the per-shard top-k lists are exchanged with ONE all-gather
+  (NCCL over NVLink on the box, gloo in the CPU tests) and merged by the K8
+  kernel (cagra_merge_shard_topk_dev): shard offsets turn local ids into
+  global ids, order (dist, id) as merge_team_results (engine.cpp:24-34).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import capi, fodg
+
+
+def shard_bounds(n: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous, balanced [start, end) id ranges (first n % world shards one longer)."""
+    if world < 1 or n < world:
+        raise fodg.UsageError("shard_bounds: need 1 <= world <= n")
+    base, extra = divmod(n, world)
+    out, s = [], 0
+    for r in range(world):
+        e = s + base + (1 if r < extra else 0)
+        out.append((s, e))
+        s = e
+    return out
+
+
+def query_slice(nq: int, world: int, rank: int) -> Tuple[int, int]:
+    """[start, end) of this rank's queries; start is the rank's query_offset."""
+    return shard_bounds(nq, world)[rank] if nq >= world else ((0, nq) if rank == 0 else (nq, nq))
+
+
+def exchange_topk(ids, dists, group=None):
+    """All-gather of every rank's [nq, k] (ids, dists): returns [G, nq, k]
+    tensors on every rank.  The one data-path collective of the
+    dataset-sharded layout (NCCL on device tensors, gloo on CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    gd = [torch.empty_like(dists) for _ in range(world)]
+    dist.all_gather(gi, ids.contiguous(), group=group)
+    dist.all_gather(gd, dists.contiguous(), group=group)
+    return torch.stack(gi), torch.stack(gd)
+
+
+def merge_shard_topk(stacked_ids, stacked_dists, offsets, device: int = 0, stream: int = 0):
+    """K8 on the device: [G, nq, k] local (ids, dists) + shard offsets -> global
+    top-k [nq, k] by (dist, global id)."""
+    import torch
+
+    G, nq, k = stacked_ids.shape
+    out_i = torch.empty((nq, k), dtype=torch.int32, device=stacked_ids.device)
+    out_d = torch.empty((nq, k), dtype=torch.float32, device=stacked_ids.device)
+    offs = np.ascontiguousarray(np.asarray(offsets, np.uint64))
+    capi.check(capi.lib().cagra_merge_shard_topk_dev(
+        capi.ptr(stacked_ids.contiguous()), capi.ptr(stacked_dists.contiguous()), G, nq, k,
+        capi.ptr(offs), capi.ptr(out_i), capi.ptr(out_d), device, C.c_void_p(stream)))
+    return out_i, out_d
+
+
+class ShardedIndex:
+    """This rank's shard of a dataset-sharded index (ids local to the shard).
+
+    `build` constructs the shard graph on this rank's GPU (exact kNN + rank
+    optimize over the shard's rows only)."""
+
+    def __init__(self, data_shard: np.ndarray, graph: fodg.Graph, offset: int, device: int = 0):
+        self.offset = int(offset)
+        self.device = device
+        self.index = fodg.Index(fodg.Dataset.from_array(data_shard), graph, device)
+
+    @classmethod
+    def build(cls, data_shard: np.ndarray, offset: int, degree: int, device: int = 0):
+        ds = fodg.Dataset.from_array(data_shard)
+        g, _ = fodg.build_graph(ds, degree, device=device)
+        return cls(data_shard, g, offset, device)
+
+    def search_local(self, d_queries, nq: int, params: fodg.SearchParams,
+                     opts: Optional[fodg.EngineOptions] = None, stream: int = 0):
+        """Per-shard search of device-resident queries (row stride = index.ld)."""
+        import torch
+
+        opts = opts or fodg.EngineOptions(device=self.device)
+        dev = torch.device("cuda", self.device)
+        ids = torch.empty((nq, params.k), dtype=torch.int32, device=dev)
+        dists = torch.empty((nq, params.k), dtype=torch.float32, device=dev)
+        self.index.search_dev(d_queries, nq, params, opts, ids, dists, None, None, stream)
+        return ids, dists
+
+    def search(self, d_queries, nq: int, params: fodg.SearchParams, offsets: List[int],
+               opts: Optional[fodg.EngineOptions] = None, group=None, stream: int = 0):
+        """Global top-k for every query on every rank: local search, one
+        all-gather of the per-shard lists, K8 merge."""
+        import torch
+
+        ids, dists = self.search_local(d_queries, nq, params, opts, stream)
+        torch.cuda.current_stream(self.device).synchronize()
+        gi, gd = exchange_topk(ids, dists, group)
+        return merge_shard_topk(gi, gd, offsets, self.device, stream)
