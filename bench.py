@@ -278,6 +278,17 @@ def run_ours(args):
     t0 = time.perf_counter()
     g, binfo = fodg.build_graph(ds, args.degree, device=local)
     build_wall = time.perf_counter() - t0
+    kst = capi.knn_last_stats()
+    kp = -(-(3 * args.dim + 6) // 64) * 64
+    # bf16 tensor-core work of the kNN build: sample pass (1/16) + full pass,
+    # 2*N*N*Kp each (Kp = 3*dim + 6 padded to 64: bf16x3 split + folded norms)
+    tc_flops = 2.0 * args.n * args.n * kp * (1 + 1 / 16)
+    knn_stats = {"path": "tcgen05 bf16x3 GEMM + exact re-rank (bit-exact)",
+                 "tensor_tflops": tc_flops / binfo["knn_seconds"] / 1e12,
+                 "fp32_equiv_tflops": 2.0 * args.n * args.n * args.dim / binfo["knn_seconds"] / 1e12,
+                 "rows": kst["rows"], "fallback_rows": kst["fallback_rows"],
+                 "retried_rows": kst["retried_rows"],
+                 "reranked_per_row": kst["reranked"] / max(1, kst["rows"])}
     gt, _ = fodg.exact_topk_batch(ds, queries, 10, device=local)
     ix = fodg.Index(ds, g, device=local)
     prm = search_params(args)
@@ -417,6 +428,7 @@ def run_ours(args):
             "mean_iterations": float(iters.mean()),
             "graph_build_s": {"knn": binfo["knn_seconds"], "optimize": binfo["optimize_seconds"],
                               "wall": build_wall},
+            "knn_build": knn_stats,
             "e2e": {"value": world * nq * args.steps / e2e_s, "unit": "queries/s",
                     "h2d_bytes_per_step": nq * args.dim * 4,
                     "d2h_bytes_per_step": nq * k * 8},

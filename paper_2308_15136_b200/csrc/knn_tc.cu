@@ -139,10 +139,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                             ((uint32_t)(TC_BM >> 4) << 24);
 
-__device__ unsigned long long g_tc_dbg[8];
-
 struct TcArgs {
-  uint32_t nq, n, kblocks, KC, exclude_self, stages, dbg;
+  uint32_t nq, n, kblocks, KC, exclude_self, stages;
   uint32_t mode;        // 0: running sorted list of KC keys; 1: append d~ <= fixed tau
   uint32_t col_stride;  // B row c is data point c * col_stride (sample pass)
   uint64_t* lists;      // mode 0: nq * KC sorted keys (dist bits << 32 | id)
@@ -289,10 +287,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     auto flush = [&](uint32_t min_cnt) {
       __syncwarp();
       unsigned todo = __ballot_sync(0xffffffffu, cnt > min_cnt);
-      if (P.dbg == 3 && lane == 0) {
-        atomicAdd(&g_tc_dbg[0], 1ull);
-        atomicAdd(&g_tc_dbg[1], (unsigned long long)__popc(todo));
-      }
       while (todo) {
         const int r = __ffs(todo) - 1;
         todo &= todo - 1;
@@ -339,12 +333,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       }
       __syncwarp();
     };
-    long long t_start = clock64(), t_wait = 0;
     for (uint32_t t = 0; t < ntiles; ++t) {
       const uint32_t acc = t % TC_ACC, aph = (t / TC_ACC) & 1;
-      long long tw = clock64();
       mbar_wait(tfull0 + 8 * acc, aph);
-      t_wait += clock64() - tw;
       tc_fence_after();
 #pragma unroll 1
       for (uint32_t c = 0; c < TC_BN / 32; ++c) {
@@ -355,7 +346,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           tc_fence_before();
           mbar_arrive(tempty0 + 8 * acc);
         }
-        if (P.dbg == 1) continue;
         // fast path: the chunk's minimum against the threshold (FMNMX3 tree)
         float m3[11];
 #pragma unroll
@@ -410,10 +400,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     } else {
       spill();
       if (live) P.bcount[row] = gcnt;
-    }
-    if (P.dbg == 3 && lane == 0) {
-      atomicAdd(&g_tc_dbg[5], (unsigned long long)(clock64() - t_start));
-      atomicAdd(&g_tc_dbg[6], (unsigned long long)t_wait);
     }
   }
   __syncthreads();
@@ -748,7 +734,7 @@ namespace {
 // Everything one kNN / top-k call shares between its passes.
 struct TcCall {
   const float* data;
-  uint32_t n, ld, dim, K, Kp, kblocks, stages, dbg;
+  uint32_t n, ld, dim, K, Kp, kblocks, stages;
   bool exclude_self;
   float eps_rel, eps_norm;
   const uint32_t* maxnorm;
@@ -760,7 +746,6 @@ void run_tc_kernel(const TcCall& c, const CUtensorMap& tmA, const CUtensorMap& t
                    uint32_t nq) {
   a.kblocks = c.kblocks;
   a.stages = c.stages;
-  a.dbg = c.dbg;
   a.exclude_self = c.exclude_self ? 1 : 0;
   a.nq = nq;
   size_t smem = tc_smem_bytes(c.kblocks, c.stages);
@@ -768,19 +753,6 @@ void run_tc_kernel(const TcCall& c, const CUtensorMap& tmA, const CUtensorMap& t
                                       (int)smem));
   knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
   CAGRA_LAUNCH_CHECK();
-}
-
-void dbg_report(const TcCall& c, const char* what, uint32_t nq) {
-  if (c.dbg != 3) return;
-  unsigned long long h[8];
-  CAGRA_CUDA_TRY(cudaStreamSynchronize(c.stream));
-  CAGRA_CUDA_TRY(cudaMemcpyFromSymbol(h, g_tc_dbg, sizeof(h)));
-  fprintf(stderr,
-          "tc dbg [%s]: flush events %llu row-flushes %llu slow chunks %llu (warps %u) "
-          "cycles: flush %llu total %llu wait-tfull %llu\n",
-          what, h[0], h[1], h[3], (nq + 127) / 128 * 4, h[4], h[5], h[6]);
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  CAGRA_CUDA_TRY(cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)));
 }
 
 // Rows [0, nq) of the query side P (bf16, Kp wide; norms qnorm; fp32 rows
@@ -803,7 +775,6 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   a.lists = lists.as<uint64_t>();
   a.self_ids = self_ids;
   run_tc_kernel(c, tmA, tmB, a, nq);
-  dbg_report(c, "list", nq);
   uint32_t* fail_cnt = fails.as<uint32_t>();
   uint32_t* fail_rows = fail_cnt + 1;
   tc_rerank_kernel<<<(nq + 7) / 8, 256, 0, c.stream>>>(
@@ -860,8 +831,6 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   c.Kp = round_up_u32(3 * dim + 6, TC_BK);
   c.kblocks = c.Kp / TC_BK;
   c.stages = tc_stages(c.kblocks);
-  const char* dbg = std::getenv("CAGRA_TC_DEBUG");
-  c.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
   c.exclude_self = exclude_self;
   c.stream = stream;
   // error bound of d~ (file header): |d~ - d| <= eps_rel |q| max|x| +
@@ -917,7 +886,6 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     a.col_stride = kSampleStride;
     a.lists = lists1.as<uint64_t>();
     run_tc_kernel(c, tmA, tmS, a, nq);
-    dbg_report(c, "sample", nq);
     // pass 2: every point with d~ <= tau* appended (no merging)
     TcArgs b{};
     b.n = n;
@@ -930,7 +898,6 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     b.bcount = bcount.as<uint32_t>();
     b.capg = capg;
     run_tc_kernel(c, tmA, tmB, b, nq);
-    dbg_report(c, "append", nq);
     uint32_t* fail_cnt = fails.as<uint32_t>();
     uint32_t* fail_rows = fail_cnt + 1;
     tc_rerank_append_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
