@@ -66,7 +66,9 @@ struct KParams {
   uint32_t k, M, p, C, max_iter, min_iter, policy, reset_interval;
   uint32_t hcap;  // visited capacity (power of two)
   uint32_t teams;  // shared mode team count (1 for per-query)
-  const uint32_t* init_ids;  // [nq][teams*C]
+  const uint32_t* init_ids;  // [nq][teams*C]; null: generated in-kernel (small C)
+  uint64_t seed, query_offset;
+  uint32_t seed_mode;
   unsigned long long* gtables;  // [grid][hcap] when the table is global
   uint32_t* gens;               // [grid]
   uint32_t* work;               // query counter
@@ -361,7 +363,10 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
       qr[c] = ch < nchunk ? reinterpret_cast<const float4*>(S.q)[ch] : make_float4(0, 0, 0, 0);
     }
     // rows in flight per team (register budget ~9-12 float4 per lane)
-    constexpr int U = MAXC <= 2 ? 4 : (MAXC == 3 ? 3 : 2);
+#ifndef CAGRA_EVAL_U3
+#define CAGRA_EVAL_U3 3
+#endif
+    constexpr int U = MAXC <= 2 ? 4 : (MAXC == 3 ? CAGRA_EVAL_U3 : 2);
     // warp-uniform trip count: every lane runs every iteration (the team
     // shuffles below use the full mask)
     for (uint32_t base = 0; base < nev; base += NTEAMS * U) {
@@ -607,7 +612,27 @@ search_kernel(const KParams P) {
 
     uint64_t* top = S.topA;
     uint64_t* nxt = S.topB;
-    const uint32_t* init = P.init_ids + (size_t)qi * P.C;
+    const uint32_t* init;
+    if (P.init_ids) {
+      init = P.init_ids + (size_t)qi * P.C;
+    } else {
+      // init samples in-kernel (search.cpp:192-201 with the engine's seeds,
+      // engine.cpp:56, 108): one sequential splitmix chain, C <= 256
+      uint32_t* buf = reinterpret_cast<uint32_t*>(S.surv);
+      if (tid == 0) {
+        const uint64_t qseed =
+            P.seed_mode == 0 ? mix_seed(P.seed ^ (0x0badull + P.query_offset + qreal)) : P.seed;
+        const uint32_t team = P.mc_teams ? qi % P.mc_teams : 0;
+        const uint64_t tseed = P.mc_teams ? mix_seed(qseed + 0x7ea4ull * (team + 1)) : qseed;
+        uint64_t state = mix_seed(tseed ^ 0x5eedull);
+        for (uint32_t j = 0; j < P.C; ++j) {
+          state = mix_seed(state);
+          buf[j] = (uint32_t)(state % P.n);
+        }
+      }
+      __syncthreads();
+      init = buf;
+    }
 
     // visit(): candidates [src 0..cnt) -> evlist of first visits
     auto visit = [&](const uint32_t* src_ids, bool from_graph, uint32_t cnt) {
@@ -633,7 +658,7 @@ search_kernel(const KParams P) {
                              : __ldg(&P.graph[(size_t)S.parents[j / P.degree] * P.degree +
                                               j % P.degree]);
               } else {
-                ids[k] = __ldg(&src_ids[j]);
+                ids[k] = src_ids[j];  // global (init_samples_kernel) or shared (in-kernel)
               }
             }
           }
@@ -1400,11 +1425,19 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
                        unsigned long long* d_team_out, void* d_team_stats, uint32_t mc_tag,
                        cudaStream_t stream) {
   if (nq == 0) return 0;
-  dim3 ig((nq + 127) / 128, pl.teams);
-  init_samples_kernel<<<ig, 128, 0, stream>>>(nq, pl.teams > 1 ? ix.degree : pl.C, pl.teams,
-                                              ix.n, c.seed, c.seed_mode, c.query_offset,
-                                              d_init_ids);
-  CAGRA_LAUNCH_CHECK();
+  // small per-item sample counts are generated inside the search kernel (one
+  // launch less on the batch-1 path); the lockstep shared kernel and large
+  // candidate lists use the batched sampler
+  const bool sample_in_kernel = c.mode != 1 ? pl.C <= 256 : pl.mc;
+  uint32_t launches = 1;
+  if (!sample_in_kernel) {
+    dim3 ig((nq + 127) / 128, pl.teams);
+    init_samples_kernel<<<ig, 128, 0, stream>>>(nq, pl.teams > 1 ? ix.degree : pl.C, pl.teams,
+                                                ix.n, c.seed, c.seed_mode, c.query_offset,
+                                                d_init_ids);
+    CAGRA_LAUNCH_CHECK();
+    ++launches;
+  }
   CAGRA_CUDA_TRY(cudaMemsetAsync(d_work, 0, sizeof(uint32_t), stream));
   KParams P;
   P.data = ix.data;
@@ -1430,7 +1463,10 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.mc_tag = mc_tag;
   P.team_out = d_team_out;
   P.team_stats = reinterpret_cast<DevStats*>(d_team_stats);
-  P.init_ids = d_init_ids;
+  P.init_ids = sample_in_kernel ? nullptr : d_init_ids;
+  P.seed = c.seed;
+  P.query_offset = c.query_offset;
+  P.seed_mode = c.seed_mode;
   P.gtables = d_tables;
   P.gens = d_gens;
   P.work = d_work;
@@ -1450,7 +1486,6 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(pl.fn));
   fn<<<pl.grid, SNT, pl.smem, stream>>>(P);
   CAGRA_LAUNCH_CHECK();
-  uint32_t launches = 2;
   if (pl.mc) {
     const uint32_t total = pl.teams * c.topm;
     const uint32_t P2 = std::max(256u, next_pow2_u32(total));
@@ -1462,7 +1497,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
         ix.data, ix.ld, ix.dim, d_queries, c.exact, d_ids, d_dists, d_counts,
         reinterpret_cast<DevStats*>(d_stats));
     CAGRA_LAUNCH_CHECK();
-    launches = 3;
+    ++launches;
   }
   if (P.prof) {
     unsigned long long h[8];

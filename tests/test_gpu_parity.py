@@ -291,7 +291,7 @@ def test_multi_cta_shared_mode_parity(gpu, oracle, name):
         ids, dists, counts, st = ix.search(
             queries, prm, fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers,
                                              team_count=teams, multi_cta=2))
-        assert ix.last_launch_count() == 3
+        assert ix.last_launch_count() == 2  # search + team merge (samples in-kernel)
         o = oracle.batch_search(g["graph"], data, queries, make_params(k=10, topm=m, width=1,
                                                                        seed=11),
                                 mode=1, team_count=teams)
