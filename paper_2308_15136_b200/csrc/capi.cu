@@ -221,6 +221,10 @@ struct cagra_index {
   DBuf init_ids, work, q, ids, dists, counts, stats, team_out, team_stats;
   uint32_t last_launches = 0;
   uint32_t mc_tag = 0;        // generation of the multi-CTA per-query tables
+  SearchPlan plan;            // cached plan for (plan_cfg, plan_nq)
+  SearchConfig plan_cfg{};
+  uint32_t plan_nq = 0;
+  bool plan_valid = false;
   bool mc_layout = false;     // tables currently laid out per query
   ~cagra_index() { delete stream; }
 };
@@ -246,7 +250,7 @@ void validate_params(const cagra_search_params* p) {
 }
 
 SearchConfig to_config(const cagra_search_params* p, const cagra_engine_opts* o) {
-  SearchConfig c;
+  SearchConfig c{};  // zeroed padding: the plan cache compares configs bytewise
   c.k = p->k;
   c.topm = p->topm;
   c.width = p->width;
@@ -276,7 +280,17 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
   DeviceIndexView v{ix->data.as<float>(), ix->graph.as<uint32_t>(), ix->n, ix->dim, ix->ld,
                     ix->degree};
   SearchConfig c = to_config(params, opts);
-  SearchPlan pl = plan_search(v, c, nq, ix->sm_count, kTableBudget);
+  // the plan (kernel variant, grid, smem, table sizes) depends only on the
+  // configuration and the batch size: reuse it across repeated calls
+  // (batch-1 loops) instead of re-querying attributes and occupancy
+  if (!ix->plan_valid || ix->plan_nq != nq ||
+      std::memcmp(&ix->plan_cfg, &c, sizeof(SearchConfig)) != 0) {
+    ix->plan = plan_search(v, c, nq, ix->sm_count, kTableBudget);
+    ix->plan_cfg = c;
+    ix->plan_nq = nq;
+    ix->plan_valid = true;
+  }
+  const SearchPlan& pl = ix->plan;
   ix->init_ids.ensure(sizeof(uint32_t) * std::max<size_t>(pl.init_elems, 1));
   ix->work.ensure(sizeof(uint32_t));
   if (pl.mc) {

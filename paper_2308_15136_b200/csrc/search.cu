@@ -81,6 +81,7 @@ struct KParams {
   // multi-CTA shared mode: work item qi = query * mc_teams + team; the teams
   // of a query share the HBM visited region of the query (generation mc_tag)
   uint32_t mc_teams, mc_tag;
+  uint32_t* mc_tab;  // [nq][hcap] u32, kInvalidId = empty, cleared per call
   unsigned long long* team_out;  // [nq * teams][M] team top-M keys
   DevStats* team_stats;          // [nq * teams]
 };
@@ -669,6 +670,7 @@ search_kernel(const KParams P) {
             bool ins = false;
             if (j < cnt)
               ins = SMEM_TABLE ? smem_insert(S.table, mask, ids[k])
+                  : P.mc_teams ? smem_insert(P.mc_tab + (size_t)qreal * P.hcap, mask, ids[k])
                                : gtab_insert(gtab, mask, tag, ids[k]);
             const uint32_t pos = warp_append_slot(&ctl.nev, ins);
             if (ins) {
@@ -1461,6 +1463,9 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.teams = pl.mc ? 1 : pl.teams;
   P.mc_teams = pl.mc ? pl.teams : 0;
   P.mc_tag = mc_tag;
+  P.mc_tab = pl.mc ? reinterpret_cast<uint32_t*>(d_tables) : nullptr;
+  if (pl.mc)  // one visited region per query, emptied for this call (one CAS per insert)
+    CAGRA_CUDA_TRY(cudaMemsetAsync(d_tables, 0xff, sizeof(uint32_t) * (size_t)nq * pl.hcap, stream));
   P.team_out = d_team_out;
   P.team_stats = reinterpret_cast<DevStats*>(d_team_stats);
   P.init_ids = sample_in_kernel ? nullptr : d_init_ids;
