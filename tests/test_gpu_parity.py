@@ -425,3 +425,40 @@ def test_search_random_params_vs_oracle(gpu, oracle):
             assert np.array_equal(st_["distance_evals"], o_st["distance_evals"]), tag
             assert np.array_equal(st_["iterations"], o_st["iterations"]), tag
             assert np.array_equal(st_["hash_resets"], o_st["hash_resets"]), tag
+
+
+# ------------------------------------------------- GIST-shaped (C3) parity ----
+def test_gist_shape_960d_pipeline_vs_oracle(gpu, oracle):
+    """BASELINE configs[2] shape (960-d, graph degree 64, multi-CTA small
+    batch) at oracle-checkable size: the kNN graph (SIMT sequential-chain path:
+    K = 3*960+6 exceeds the tensor-core tile) and the optimized graph are
+    bit-exact; per-query search in reference-semantics mode matches the oracle
+    exactly; multi-CTA shared mode is within 0.5 pp of the reference's shared
+    mode."""
+    n, dim, nq, d = 3000, 960, 40, 64
+    data = oracle.uniform_dataset(n, dim, 31)
+    queries = oracle.uniform_dataset(nq, dim, 32)
+    ds = fodg.Dataset.from_array(data)
+    g, _, knn = fodg.build_graph(ds, d, 2 * d, return_knn=True)
+    o_ids, o_d = oracle.exact_knn_graph(data, 2 * d)
+    assert np.array_equal(knn.ids, o_ids)
+    assert np.array_equal(bits(knn.dists), bits(o_d))
+    o_graph = oracle.optimize(o_ids, o_d, d)
+    assert np.array_equal(g.ids, o_graph)
+    ix = fodg.Index(ds, g)
+    prm = fodg.SearchParams(k=10, topm=64, width=2, seed=5)
+    ids, dists, _, st = ix.search(queries, prm, fodg.EngineOptions(exact_distances=True))
+    o = oracle.batch_search(o_graph, data, queries, make_params(k=10, topm=64, width=2, seed=5))
+    assert np.array_equal(ids, o[0])
+    assert np.array_equal(bits(dists), bits(o[1]))
+    assert np.array_equal(st["distance_evals"], o[3]["distance_evals"])
+    gt, _ = fodg.exact_topk_batch(ds, queries, 10)
+    sp = fodg.SearchParams(k=10, topm=32, width=1, seed=5)
+    mc = ix.search(queries, sp, fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers,
+                                                   team_count=8, multi_cta=2))[0]
+    ref = oracle.batch_search(o_graph, data, queries, make_params(k=10, topm=32, width=1,
+                                                                  seed=5), mode=1,
+                              team_count=8)[0]
+    rec = np.mean([len(set(mc[q]) & set(gt[q])) / 10 for q in range(nq)])
+    ref_rec = np.mean([len(set(ref[q]) & set(gt[q])) / 10 for q in range(nq)])
+    assert abs(rec - ref_rec) <= 0.005 + 1e-9, (rec, ref_rec)
