@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--points", dest="n", type=int, default=1_000_000)
     ap.add_argument("--dim", type=int, default=96)
     ap.add_argument("--batch", type=int, default=10_000)
     ap.add_argument("--degree", type=int, default=64)
@@ -267,9 +267,16 @@ def run_ours(args):
     from paper_2308_15136_b200 import capi, fodg
 
     world, rank, local = dist_env()
+    # one process per GPU; CAGRA_BENCH_BACKEND=gloo lets several ranks share a
+    # device (exercises the N>1 path on a 1-GPU box; NCCL needs distinct GPUs)
+    backend = os.environ.get("CAGRA_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
