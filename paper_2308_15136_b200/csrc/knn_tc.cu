@@ -53,8 +53,9 @@ namespace {
 constexpr int TC_BM = 128;    // query rows per CTA (= TMEM lanes)
 constexpr int TC_BN = 128;    // data points per tile (= accumulator columns)
 constexpr int TC_BK = 64;     // bf16 per K-block (128 B rows, SWIZZLE_128B)
-constexpr int TC_STAGES = 4;  // B ring depth
-constexpr int TC_PEND = 48;   // pending keys per row in smem
+constexpr int TC_STAGES = 8;  // max B ring depth (as smem allows)
+constexpr int TC_PEND = 48;   // pending keys per row in smem (list mode)
+constexpr int TC_PEND_APPEND = 32;  // append mode: spills are cheap, smem goes to the TMA ring
 constexpr int TC_THREADS = 192;  // w0 TMA, w1 MMA, w2..w5 epilogue
 constexpr int TC_ACC = 4;        // TMEM accumulator ring (4 x 128 columns = all 512)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
@@ -140,7 +141,7 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
                             ((uint32_t)(TC_BM >> 4) << 24);
 
 struct TcArgs {
-  uint32_t nq, n, kblocks, KC, exclude_self, stages;
+  uint32_t nq, n, kblocks, KC, exclude_self, stages, pend_cap;
   uint32_t mode;        // 0: running sorted list of KC keys; 1: append d~ <= fixed tau
   uint32_t col_stride;  // B row c is data point c * col_stride (sample pass)
   uint64_t* lists;      // mode 0: nq * KC sorted keys (dist bits << 32 | id)
@@ -161,7 +162,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   unsigned char* sA = base;                                   // kblocks x 16 KB
   unsigned char* sB = sA + (size_t)P.kblocks * TILE_BYTES;    // stages x 16 KB
   uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * TILE_BYTES);  // PEND x 128
-  float* scratch = reinterpret_cast<float*>(pend + TC_PEND * TC_BM);  // 128 rows x 33
+  float* scratch = reinterpret_cast<float*>(pend + P.pend_cap * TC_BM);  // 128 rows x 33
   uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + TC_BM * 33 + 8);
   // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * TC_ACC);
@@ -389,7 +390,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
               make_key(fmaxf(scratch[rl * 33 + i], 0.0f), (cbase + i) * P.col_stride);
           ++cnt;
         }
-        if (__any_sync(0xffffffffu, cnt > TC_PEND - 32)) {
+        if (__any_sync(0xffffffffu, cnt > P.pend_cap - 32)) {
           if (P.mode == 0) flush(TC_PEND / 4);
           else spill();
         }
@@ -703,17 +704,18 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_
   return tm;
 }
 
-size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages) {
+size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_PEND) {
   return 1024 + (size_t)kblocks * TILE_BYTES + stages * TILE_BYTES +
-         sizeof(uint64_t) * (TC_PEND * TC_BM + 2 * stages + 1 + 2 * TC_ACC) +
+         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * TC_ACC) +
          sizeof(float) * (TC_BM * 33 + 8) + 16;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-uint32_t tc_stages(uint32_t kblocks) {
+// deepest B ring that fits next to the resident query tile
+uint32_t tc_stages(uint32_t kblocks, uint32_t pend_cap = TC_PEND) {
   uint32_t s = TC_STAGES;
-  while (s > 2 && tc_smem_bytes(kblocks, s) > kSmemLimit) --s;
+  while (s > 2 && tc_smem_bytes(kblocks, s, pend_cap) > kSmemLimit) --s;
   return s;
 }
 
@@ -745,10 +747,11 @@ struct TcCall {
 void run_tc_kernel(const TcCall& c, const CUtensorMap& tmA, const CUtensorMap& tmB, TcArgs a,
                    uint32_t nq) {
   a.kblocks = c.kblocks;
-  a.stages = c.stages;
+  a.pend_cap = a.mode == 1 ? TC_PEND_APPEND : TC_PEND;
+  a.stages = tc_stages(c.kblocks, a.pend_cap);
   a.exclude_self = c.exclude_self ? 1 : 0;
   a.nq = nq;
-  size_t smem = tc_smem_bytes(c.kblocks, c.stages);
+  size_t smem = tc_smem_bytes(c.kblocks, a.stages, a.pend_cap);
   CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
