@@ -57,7 +57,14 @@ constexpr int TC_STAGES = 8;  // max B ring depth (as smem allows)
 constexpr int TC_PEND = 48;   // pending keys per row in smem (list mode)
 constexpr int TC_PEND_APPEND = 32;  // append mode: spills are cheap, smem goes to the TMA ring
 constexpr int TC_THREADS = 192;  // w0 TMA, w1 MMA, w2..w5 epilogue
-constexpr int TC_ACC = 4;        // TMEM accumulator ring (4 x 128 columns = all 512)
+// A (the CTA's query tile, constant for the whole sweep) lives in TMEM and the
+// MMA reads it from there (tcgen05.mma ... [a_tmem]): shared memory only
+// feeds B, halving the operand traffic that bounds the SS form.
+#ifndef CAGRA_KNN_TS
+#define CAGRA_KNN_TS 1
+#endif
+constexpr int TC_ACC = CAGRA_KNN_TS ? 2 : 4;  // TMEM accumulator ring (x 128 columns)
+constexpr uint32_t TC_A_COL = 2 * 128;         // TS: A at TMEM columns [256, 256 + Kp/2)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
 constexpr uint32_t TILE_BYTES = TC_BN * TC_BK * 2;  // 16 KB
 
@@ -111,6 +118,29 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] . B[smem]^T (A: lane = row, 2 bf16 per 32-bit column).
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive columns <- 32 registers per thread.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -151,6 +181,8 @@ struct TcArgs {
   uint32_t* bcount;     // mode 1: keys appended per row (capg + 1 = overflow)
   uint32_t capg;
   const uint32_t* self_ids;  // optional: data id of each query row (self exclusion)
+  const uint32_t* prow;      // TS: query-side rows (nq x Kp bf16, as Kp/2 u32) for TMEM
+  uint32_t groups;           // CTAs start their sweep at one of `groups` evenly spaced tiles
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -159,11 +191,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B tiles
   unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
-  unsigned char* sA = base;                                   // kblocks x 16 KB
-  unsigned char* sB = sA + (size_t)P.kblocks * TILE_BYTES;    // stages x 16 KB
+  unsigned char* sA = base;                                   // SS: kblocks x 16 KB
+  unsigned char* sB = sA + (CAGRA_KNN_TS ? 0 : (size_t)P.kblocks * TILE_BYTES);  // stages x 16 KB
   uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * TILE_BYTES);  // PEND x 128
-  float* scratch = reinterpret_cast<float*>(pend + P.pend_cap * TC_BM);  // 128 rows x 33
-  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + TC_BM * 33 + 8);
+  uint64_t* bars = pend + P.pend_cap * TC_BM;
   // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * TC_ACC);
 
@@ -174,13 +205,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
   const uint32_t afull = smem_u32(bars + 2 * S);
   const uint32_t tfull0 = afull + 8, tempty0 = afull + 8 + 8 * TC_ACC;
+  // Staggered sweep: CTAs of group g start at tile g*ntiles/groups, so the
+  // resident CTAs spread their B-tile reads over `groups` regions of L2
+  // instead of all hitting the same lines (results do not depend on order).
+  const uint32_t start_tile =
+      P.groups > 1 ? (uint32_t)(((uint64_t)(blockIdx.x % P.groups) * ntiles) / P.groups) : 0u;
+  auto tile_of = [&](uint32_t t) {
+    const uint32_t x = t + start_tile;
+    return x >= ntiles ? x - ntiles : x;
+  };
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(afull, 1);
+    mbar_init(afull, CAGRA_KNN_TS ? 128 : 1);  // TS: the 128 epilogue threads write A
     for (int a = 0; a < TC_ACC; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 128);
@@ -203,9 +243,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      mbar_expect_tx(afull, P.kblocks * TILE_BYTES);
-      for (uint32_t kb = 0; kb < P.kblocks; ++kb)
-        tma_load_2d(smem_u32(sA + kb * TILE_BYTES), &tmA, afull, kb * TC_BK, row0);
+      if (!CAGRA_KNN_TS) {
+        mbar_expect_tx(afull, P.kblocks * TILE_BYTES);
+        for (uint32_t kb = 0; kb < P.kblocks; ++kb)
+          tma_load_2d(smem_u32(sA + kb * TILE_BYTES), &tmA, afull, kb * TC_BK, row0);
+      }
       uint32_t it = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
         for (uint32_t kb = 0; kb < P.kblocks; ++kb, ++it) {
@@ -213,7 +255,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           mbar_wait(empty0 + 8 * s, ph ^ 1);
           mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
           tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
-                      t * TC_BN);
+                      tile_of(t) * TC_BN);
         }
       }
     }
@@ -232,11 +274,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
-          const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
           const uint64_t bd = sw128_desc(smem_u32(sB + s * TILE_BYTES));
+#if CAGRA_KNN_TS
+#pragma unroll
+          for (uint32_t k = 0; k < TC_BK / 16; ++k)  // A: 16 bf16 = 8 TMEM columns per step
+            tc_mma_ts(dcol, tmem + TC_A_COL + kb * (TC_BK / 2) + k * 8, bd + 2 * k, kIdesc,
+                      (kb | k) != 0);
+#else
+          const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
 #pragma unroll
           for (uint32_t k = 0; k < TC_BK / 16; ++k)  // 16 bf16 = 32 B = +2 in the address field
             tc_mma(dcol, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0);
+#endif
           tc_commit(empty0 + 8 * s);
         }
         tc_commit(tfull0 + 8 * acc);
@@ -248,6 +297,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t rl = q4 * 32 + lane;         // row within the tile
     const uint32_t row = row0 + rl;
     const bool live = row < P.nq;
+#if CAGRA_KNN_TS
+    {
+      // this row of A -> TMEM lane rl, columns [TC_A_COL, TC_A_COL + Kp/2)
+      const uint32_t half = P.kblocks * (TC_BK / 2);
+      const uint32_t* src = P.prow + (size_t)(live ? row : 0) * half;
+      for (uint32_t c0 = 0; c0 < half; c0 += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = live ? __ldg(src + c0 + i) : 0u;
+        tmem_st32(tmem + ((q4 * 32) << 16) + TC_A_COL + c0, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(afull);
+    }
+#endif
     if (P.mode == 0) {
       for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
         const uint32_t rr = row0 + q4 * 32 + r;
@@ -372,23 +437,30 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         const bool hit = live && mn <= tau_f && gcnt <= P.capg;
         if (!__any_sync(0xffffffffu, hit)) continue;
-        // slow path: stash the chunk, then walk the passing bits
-        const uint32_t cbase = t * TC_BN + c * 32;
-        uint32_t m = 0;
+        // slow path: only the FMNMX3 groups whose minimum passes are
+        // examined element by element (appends are rare after the first tiles)
+        const uint32_t cbase = tile_of(t) * TC_BN + c * 32;
         if (hit) {
+          auto take = [&](int i) {
+            const float d = __uint_as_float(v[i]);
+            const uint32_t col = cbase + i;
+            if (d <= tau_f && col < P.n && col != self_c) {
+              pend[cnt * TC_BM + rl] = make_key(fmaxf(d, 0.0f), col * P.col_stride);
+              ++cnt;
+            }
+          };
 #pragma unroll
-          for (int i = 0; i < 32; ++i) m |= (__uint_as_float(v[i]) <= tau_f ? 1u : 0u) << i;
-          if (cbase + 32 > P.n) m &= cbase >= P.n ? 0u : (1u << (P.n - cbase)) - 1u;
-          if (self_c - cbase < 32u) m &= ~(1u << (self_c - cbase));
-#pragma unroll
-          for (int i = 0; i < 32; ++i) scratch[rl * 33 + i] = __uint_as_float(v[i]);
-        }
-        while (m) {
-          const int i = __ffs(m) - 1;
-          m &= m - 1;
-          pend[cnt * TC_BM + rl] =
-              make_key(fmaxf(scratch[rl * 33 + i], 0.0f), (cbase + i) * P.col_stride);
-          ++cnt;
+          for (int g = 0; g < 10; ++g) {
+            if (m3[g] <= tau_f) {
+              take(3 * g);
+              take(3 * g + 1);
+              take(3 * g + 2);
+            }
+          }
+          if (m3[10] <= tau_f) {
+            take(30);
+            take(31);
+          }
         }
         if (__any_sync(0xffffffffu, cnt > P.pend_cap - 32)) {
           if (P.mode == 0) flush(TC_PEND / 4);
@@ -705,9 +777,8 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_
 }
 
 size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_PEND) {
-  return 1024 + (size_t)kblocks * TILE_BYTES + stages * TILE_BYTES +
-         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * TC_ACC) +
-         sizeof(float) * (TC_BM * 33 + 8) + 16;
+  return 1024 + (CAGRA_KNN_TS ? 0 : (size_t)kblocks * TILE_BYTES) + stages * TILE_BYTES +
+         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * TC_ACC) + 16;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -744,9 +815,12 @@ struct TcCall {
   cudaStream_t stream;
 };
 
-void run_tc_kernel(const TcCall& c, const CUtensorMap& tmA, const CUtensorMap& tmB, TcArgs a,
-                   uint32_t nq) {
+void run_tc_kernel(const TcCall& c, const void* Pq, const CUtensorMap& tmA,
+                   const CUtensorMap& tmB, TcArgs a, uint32_t nq) {
   a.kblocks = c.kblocks;
+  a.prow = reinterpret_cast<const uint32_t*>(Pq);
+  const char* ge = std::getenv("CAGRA_TC_GROUPS");
+  a.groups = ge ? (uint32_t)std::atoi(ge) : 1u;  // measured: the lockstep sweep wins (L2 reuse)
   a.pend_cap = a.mode == 1 ? TC_PEND_APPEND : TC_PEND;
   a.stages = tc_stages(c.kblocks, a.pend_cap);
   a.exclude_self = c.exclude_self ? 1 : 0;
@@ -777,7 +851,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   a.col_stride = 1;
   a.lists = lists.as<uint64_t>();
   a.self_ids = self_ids;
-  run_tc_kernel(c, tmA, tmB, a, nq);
+  run_tc_kernel(c, P, tmA, tmB, a, nq);
   uint32_t* fail_cnt = fails.as<uint32_t>();
   uint32_t* fail_rows = fail_cnt + 1;
   tc_rerank_kernel<<<(nq + 7) / 8, 256, 0, c.stream>>>(
@@ -888,7 +962,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     a.mode = 0;
     a.col_stride = kSampleStride;
     a.lists = lists1.as<uint64_t>();
-    run_tc_kernel(c, tmA, tmS, a, nq);
+    run_tc_kernel(c, dP.p, tmA, tmS, a, nq);
     // pass 2: every point with d~ <= tau* appended (no merging)
     TcArgs b{};
     b.n = n;
@@ -900,7 +974,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     b.bufs = bufs.as<uint64_t>();
     b.bcount = bcount.as<uint32_t>();
     b.capg = capg;
-    run_tc_kernel(c, tmA, tmB, b, nq);
+    run_tc_kernel(c, dP.p, tmA, tmB, b, nq);
     uint32_t* fail_cnt = fails.as<uint32_t>();
     uint32_t* fail_rows = fail_cnt + 1;
     tc_rerank_append_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
