@@ -421,7 +421,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args, data, g.ids, queries, gt)
+        cpu = cpu_baseline(args, data, g.ids, queries, gt, hid)
 
     if rank == 0:
         line = {
@@ -450,6 +450,8 @@ def run_ours(args):
         }
         if b1 is not None:
             line["batch1"] = b1
+        if cpu and "parity_vs_gpu" in cpu:
+            line["parity"] = cpu["parity_vs_gpu"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -457,7 +459,7 @@ def run_ours(args):
     return 0
 
 
-def cpu_baseline(args, data, graph, queries, gt):
+def cpu_baseline(args, data, graph, queries, gt, gpu_ids):
     """The reference (oracle/_ref) on the host cores: bounded query sample."""
     try:
         from oracle.bindings import load_reference, make_params
@@ -481,8 +483,17 @@ def cpu_baseline(args, data, graph, queries, gt):
     ids, _, _, _ = rix.batch_search(queries[:sample], p, threads=threads)
     el = time.perf_counter() - t0
     rix.close()
+    # parity on the same queries, same params and seeds: the GPU batch's ids
+    # (fast mode: team-reduced in-loop distances) against the reference's
+    ref_rec = recall_at_k(ids, gt[:sample])
+    gpu_rec = recall_at_k(gpu_ids[:sample], gt[:sample])
+    parity = {"queries": sample, "recall_gpu": gpu_rec, "recall_reference": ref_rec,
+              "delta_pp": 100.0 * (gpu_rec - ref_rec),
+              "exact_id_match": float(np.mean(gpu_ids[:sample] == ids)),
+              "set_overlap": float(np.mean([len(set(gpu_ids[i]) & set(ids[i])) / 10
+                                            for i in range(sample)]))}
     return {"value": sample / el, "unit": "queries/s", "cores": threads, "kind": "reference",
-            "recall@10": recall_at_k(ids, gt[:sample]),
+            "recall@10": ref_rec, "parity_vs_gpu": parity,
             "sample": f"first {sample} of the {args.batch} batch queries, same index and "
                       f"params, fodg::batch_search per-query mode, {threads} threads"}
 

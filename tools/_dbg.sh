@@ -1,3 +1,5 @@
-timeout 300 python tools/knn_check.py 0 > gpurun_out/knn_check8.log 2>&1
-python tools/knn_prof.py 1000000 >> gpurun_out/knn_check8.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -k "knn or gist or build" -q >> gpurun_out/knn_check8.log 2>&1
+python -c "import torch;print(torch.cuda.get_device_properties(0))" > gpurun_out/l2p.log 2>&1
+for f in none 0.5 0.75; do
+  if [ $f = none ]; then unset CAGRA_L2_PERSIST; else export CAGRA_L2_PERSIST=$f; fi
+  python tools/sweep.py --grid '896,16,1,12,0,1' 2>&1 | grep "M=" | sed "s/^/persist=$f /" >> gpurun_out/l2p.log
+done
