@@ -963,13 +963,25 @@ team_merge_kernel(const unsigned long long* __restrict__ team_out,
   __syncthreads();
   const uint32_t live = nfin;
   if (!exact) {
+    // sequential-chain re-score: each warp stages a candidate row and the
+    // query in shared memory with coalesced loads, then one lane runs the
+    // chain from smem (a per-dimension dependent global load would dominate)
+    float* rowbuf = reinterpret_cast<float*>(fin + 256) + warp * 2 * ld;
     const float* qv = queries + (size_t)q * ld;
-    for (uint32_t i = tid; i < live; i += SNT) {
+    for (uint32_t i = warp; i < live; i += SNT / 32) {
       const uint32_t id = key_id(fin[i]);
       const float* x = data + (size_t)id * ld;
-      float acc = 0.0f;
-      for (uint32_t d = 0; d < dim; ++d) acc = seq_step(acc, __ldg(x + d), __ldg(qv + d));
-      fin[i] = make_key(acc, id);
+      for (uint32_t j = lane; j < ld; j += 32) {
+        rowbuf[j] = __ldg(x + j);
+        rowbuf[ld + j] = __ldg(qv + j);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        float acc = 0.0f;
+        for (uint32_t d = 0; d < dim; ++d) acc = seq_step(acc, rowbuf[d], rowbuf[ld + d]);
+        fin[i] = make_key(acc, id);
+      }
+      __syncwarp();
     }
     __syncthreads();
     if (warp == 0) warp_sort_smem(fin, live, lane);
@@ -1494,7 +1506,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   if (pl.mc) {
     const uint32_t total = pl.teams * c.topm;
     const uint32_t P2 = std::max(256u, next_pow2_u32(total));
-    const size_t msmem = 8ull * (P2 + 256);
+    const size_t msmem = 8ull * (P2 + 256) + sizeof(float) * 2 * ix.ld * (SNT / 32);
     CAGRA_CUDA_TRY(cudaFuncSetAttribute(team_merge_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
     team_merge_kernel<<<nq, SNT, msmem, stream>>>(
