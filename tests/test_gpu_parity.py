@@ -462,3 +462,44 @@ def test_gist_shape_960d_pipeline_vs_oracle(gpu, oracle):
     rec = np.mean([len(set(mc[q]) & set(gt[q])) / 10 for q in range(nq)])
     ref_rec = np.mean([len(set(ref[q]) & set(gt[q])) / 10 for q in range(nq)])
     assert abs(rec - ref_rec) <= 0.005 + 1e-9, (rec, ref_rec)
+
+
+# ------------------------------------------------------------- edge cases ----
+@pytest.mark.parametrize("n,dim,d,m,p,k,pol", [
+    (40, 1, 4, 8, 1, 8, 0),        # 1-D, k == M, tiny graph
+    (130, 7, 6, 16, 3, 5, 1),      # odd dim, degree 6 (not a power of two), forgettable
+    (257, 33, 12, 24, 2, 24, 0),   # k == M, ragged sizes
+    (600, 8, 24, 64, 5, 10, 1),    # degree 24, p*d = 120 candidates
+])
+def test_search_edge_shapes_reference_semantics(gpu, oracle, n, dim, d, m, p, k, pol):
+    data = oracle.uniform_dataset(n, dim, n + dim)
+    queries = oracle.uniform_dataset(11, dim, 3)
+    ids_k, d_k = oracle.exact_knn_graph(data, 2 * d)
+    graph = oracle.optimize(ids_k, d_k, d)
+    ix = fodg.Index(fodg.Dataset.from_array(data), fodg.Graph(n, d, graph))
+    prm = fodg.SearchParams(k=k, topm=m, width=p, hash_policy=fodg.HashPolicy(pol), hash_bits=6,
+                            seed=17)
+    ids, dists, counts, st = ix.search(queries, prm, fodg.EngineOptions(exact_distances=True))
+    o = oracle.batch_search(graph, data, queries, make_params(k=k, topm=m, width=p,
+                                                              hash_policy=pol, hash_bits=6,
+                                                              seed=17))
+    assert np.array_equal(ids, o[0])
+    assert np.array_equal(bits(dists), bits(o[1]))
+    assert np.array_equal(counts, o[2])
+    assert np.array_equal(st["distance_evals"], o[3]["distance_evals"])
+    assert np.array_equal(st["hash_resets"], o[3]["hash_resets"])
+
+
+def test_search_empty_batch_and_limits(gpu, oracle):
+    data = oracle.uniform_dataset(300, 8, 1)
+    ds = fodg.Dataset.from_array(data)
+    g = fodg.optimize(fodg.exact_knn_graph(ds, 16), 8)
+    ix = fodg.Index(ds, g)
+    ids, dists, counts, st = ix.search(np.zeros((0, 8), np.float32), fodg.SearchParams())
+    assert ids.shape == (0, 10) and counts.shape == (0,)
+    # parameters beyond the device's shared-memory budget fail loudly (UsageError)
+    with pytest.raises(fodg.UsageError):
+        ix.search(data[:2], fodg.SearchParams(k=10, topm=20000, width=64))
+    # dimension mismatch / graph-dataset mismatch, reference messages' classes
+    with pytest.raises(fodg.UsageError):
+        fodg.batch_search(g, ds, fodg.Dataset.from_array(data[:3, :4]), fodg.SearchParams())
