@@ -340,7 +340,7 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
       uint32_t t = 0;
       if (e < nev) {
         uint32_t id = S.evlist[e];
-        t = S.evteam[e];
+        t = P.teams == 1 ? 0u : S.evteam[e];
         float dist = exact_dist(P.data + (size_t)id * P.ld, S.q, P.dim);
         key = make_key(dist, id);
       }
@@ -404,7 +404,7 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
         bool keep = false;
         if (lt == 0 && e < nev) {
           uint32_t id = S.evlist[e];
-          t = S.evteam[e];
+          t = P.teams == 1 ? 0u : S.evteam[e];
           key = make_key(acc, id);
           keep = key < ctl.worst[t];
         }
@@ -445,7 +445,7 @@ __device__ __forceinline__ void eval_list_generic(const KParams& P, const Smem& 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lt == 0) {
-      uint32_t t = S.evteam[e];
+      uint32_t t = P.teams == 1 ? 0u : S.evteam[e];
       uint64_t key = make_key(acc, id);
       if (key < ctl.worst[t]) {
         uint32_t pos = atomicAdd(&ctl.nsurv[t], 1u);
@@ -543,7 +543,6 @@ __device__ void serial_visit(const KParams& P, const Smem& S, Ctl& ctl, const ui
     }
     if (r == 0) {
       S.evlist[nev] = id;
-      S.evteam[nev] = 0;
       ++nev;
     }
   }
@@ -551,8 +550,11 @@ __device__ void serial_visit(const KParams& P, const Smem& S, Ctl& ctl, const ui
 }
 
 // ------------------------------------------------------ per-query kernel ---
+#ifndef CAGRA_SEARCH_MINB
+#define CAGRA_SEARCH_MINB 4  // 64 registers: 4 CTAs (1024 threads) per SM; the heuristic alone is unstable
+#endif
 template <int TEAM, int MAXC, bool EXACT, bool SMEM_TABLE>
-__global__ void __launch_bounds__(SNT)
+__global__ void __launch_bounds__(SNT, CAGRA_SEARCH_MINB)
 search_kernel(const KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Ctl ctl;
@@ -571,8 +573,7 @@ search_kernel(const KParams P) {
     p += sizeof(uint64_t) * SP;
     S.evlist = reinterpret_cast<uint32_t*>(p);
     p += sizeof(uint32_t) * P.C;
-    S.evteam = reinterpret_cast<uint16_t*>(p);
-    p += sizeof(uint16_t) * round_up_u32(P.C, 2);
+    S.evteam = nullptr;  // one team: every candidate belongs to team 0
     S.parents = reinterpret_cast<uint32_t*>(p);
     p += sizeof(uint32_t) * round_up_u32(P.p, 4);
     S.table = reinterpret_cast<uint32_t*>(p);
@@ -673,10 +674,7 @@ search_kernel(const KParams P) {
                   : P.mc_teams ? smem_insert(P.mc_tab + (size_t)qreal * P.hcap, mask, ids[k])
                                : gtab_insert(gtab, mask, tag, ids[k]);
             const uint32_t pos = warp_append_slot(&ctl.nev, ins);
-            if (ins) {
-              S.evlist[pos] = ids[k];
-              S.evteam[pos] = 0;
-            }
+            if (ins) S.evlist[pos] = ids[k];
           }
         }
         __syncthreads();
@@ -1387,8 +1385,8 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   size_t smem;
   if (!shared) {
     uint32_t SP = std::max(256u, next_pow2_u32(C));
-    smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * C + 2ull * round_up_u32(C, 2) +
-           4ull * round_up_u32(p, 4) + (pl.smem_table ? 4ull * hcap : 0);
+    smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * C + 4ull * round_up_u32(p, 4) +
+           (pl.smem_table ? 4ull * hcap : 0);
   } else {
     if (d > 256) throw UsageErr("batch_search: shared mode on device needs graph degree <= 256");
     uint32_t SP = next_pow2_u32(d), RP = next_pow2_u32(2 * T * d), KP = next_pow2_u32(c.k);
