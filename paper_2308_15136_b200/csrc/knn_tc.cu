@@ -57,13 +57,13 @@ constexpr int TC_STAGES = 8;  // max B ring depth (as smem allows)
 constexpr int TC_PEND = 48;   // pending keys per row in smem (list mode)
 constexpr int TC_PEND_APPEND = 32;  // append mode: spills are cheap, smem goes to the TMA ring
 constexpr int TC_THREADS = 192;  // w0 TMA, w1 MMA, w2..w5 epilogue
+constexpr int TC_EPI_WARPS = 4;
 // A (the CTA's query tile, constant for the whole sweep) lives in TMEM and the
 // MMA reads it from there (tcgen05.mma ... [a_tmem]): shared memory only
 // feeds B, halving the operand traffic that bounds the SS form.
 #ifndef CAGRA_KNN_TS
 #define CAGRA_KNN_TS 1
 #endif
-constexpr int TC_ACC = CAGRA_KNN_TS ? 2 : 4;  // TMEM accumulator ring (x 128 columns)
 constexpr uint32_t TC_A_COL = 2 * 128;         // TS: A at TMEM columns [256, 256 + Kp/2)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
 constexpr uint32_t TILE_BYTES = TC_BN * TC_BK * 2;  // 16 KB
@@ -82,9 +82,69 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+#ifndef CAGRA_TC_WATCHDOG
+#define CAGRA_TC_WATCHDOG 0  // 1: trap a barrier wait that exceeds ~10 s (pipeline debugging)
+#endif
+
+// ---- CTA-pair (cluster of 2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar),
+      "r"(cta)
+      : "memory");
+}
+// 2-SM TMA: each CTA loads its share, completion counted on the LEADER's
+// barrier (peer bit cleared in the barrier address).
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* tm, uint32_t bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+// D[tmem, both CTAs] (+)= A[smem, M split over the pair] . B[smem, N split]^T
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit: arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+// Waits for the barrier phase; a wait that never completes (a pipeline bug)
+// traps after ~10 s instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
+#if CAGRA_TC_WATCHDOG
+  const long long t0 = clock64();
+#endif
   do {
+#if CAGRA_TC_WATCHDOG
+    if (clock64() - t0 > 20000000000ll) __trap();
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -178,63 +238,87 @@ struct TcArgs {
   const uint64_t* tau_keys;  // mode 1: row's threshold = key_dist(tau_keys[row * tau_ld + tau_ld - 1])
   uint32_t tau_ld;
   uint64_t* bufs;       // mode 1: nq * capg appended keys
-  uint32_t* bcount;     // mode 1: keys appended per row (capg + 1 = overflow)
+  uint32_t* bcount;     // mode 1: keys appended per row (> capg: overflow), zeroed by the host
   uint32_t capg;
   const uint32_t* self_ids;  // optional: data id of each query row (self exclusion)
   const uint32_t* prow;      // TS: query-side rows (nq x Kp bf16, as Kp/2 u32) for TMEM
   uint32_t groups;           // CTAs start their sweep at one of `groups` evenly spaced tiles
 };
 
+// PAIR: a cluster of 2 CTAs shares each data tile: every CTA keeps its own
+// 128 query rows (A, smem) and loads HALF of the 128-point B tile; the leader
+// issues tcgen05.mma.cta_group::2 (M = 256) and each CTA's TMEM receives its
+// rows x all 128 points.  Per-SM B traffic from L2 halves.
+template <bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const TcArgs P) {
+  constexpr bool TS = CAGRA_KNN_TS && !PAIR;
+  constexpr int ACC = TS ? 2 : 4;
+  constexpr uint32_t BTILE = PAIR ? TILE_BYTES / 2 : TILE_BYTES;  // B bytes per stage per CTA
+  constexpr uint32_t idesc = PAIR ? ((1u << 4) | (1u << 7) | (1u << 10) |
+                                     ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24))
+                                  : kIdesc;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B tiles
   unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
   unsigned char* sA = base;                                   // SS: kblocks x 16 KB
-  unsigned char* sB = sA + (CAGRA_KNN_TS ? 0 : (size_t)P.kblocks * TILE_BYTES);  // stages x 16 KB
-  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * TILE_BYTES);  // PEND x 128
+  unsigned char* sB = sA + (TS ? 0 : (size_t)P.kblocks * TILE_BYTES);  // stages x BTILE
+  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * BTILE);  // PEND x 128
   uint64_t* bars = pend + P.pend_cap * TC_BM;
   // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * TC_ACC);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * ACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t row0 = blockIdx.x * TC_BM;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const uint32_t row0 = PAIR ? (blockIdx.x >> 1) * 2 * TC_BM + rank * TC_BM : blockIdx.x * TC_BM;
   const uint32_t ntiles = (P.n + TC_BN - 1) / TC_BN;
   const uint32_t S = P.stages;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
   const uint32_t afull = smem_u32(bars + 2 * S);
-  const uint32_t tfull0 = afull + 8, tempty0 = afull + 8 + 8 * TC_ACC;
+  const uint32_t tfull0 = afull + 8, tempty0 = afull + 8 + 8 * ACC;
   // Staggered sweep: CTAs of group g start at tile g*ntiles/groups, so the
   // resident CTAs spread their B-tile reads over `groups` regions of L2
   // instead of all hitting the same lines (results do not depend on order).
   const uint32_t start_tile =
-      P.groups > 1 ? (uint32_t)(((uint64_t)(blockIdx.x % P.groups) * ntiles) / P.groups) : 0u;
+      !PAIR && P.groups > 1 ? (uint32_t)(((uint64_t)(blockIdx.x % P.groups) * ntiles) / P.groups)
+                            : 0u;
   auto tile_of = [&](uint32_t t) {
     const uint32_t x = t + start_tile;
     return x >= ntiles ? x - ntiles : x;
   };
 
   if (threadIdx.x == 0) {
+    // PAIR: full/afull/tempty are counted on the leader (both CTAs arrive);
+    // empty/tfull get the leader's multicast commit in each CTA
     for (uint32_t s = 0; s < S; ++s) {
-      mbar_init(full0 + 8 * s, 1);
+      mbar_init(full0 + 8 * s, PAIR ? 2 : 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(afull, CAGRA_KNN_TS ? 128 : 1);  // TS: the 128 epilogue threads write A
-    for (int a = 0; a < TC_ACC; ++a) {
+    mbar_init(afull, TS ? 4 : (PAIR ? 2 : 1));  // TS: the 4 epilogue warps write A
+    for (int a = 0; a < ACC; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 128);
+      mbar_init(tempty0 + 8 * a, (PAIR ? 2 : 1) * TC_EPI_WARPS);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -243,7 +327,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      if (!CAGRA_KNN_TS) {
+      if (PAIR) {
+        // own 128 rows of A; the leader's barrier counts both CTAs' bytes
+        for (uint32_t kb = 0; kb < P.kblocks; ++kb)
+          tma_load_2d_pair(smem_u32(sA + kb * TILE_BYTES), &tmA, afull, kb * TC_BK, row0);
+        if (leader) mbar_expect_tx(afull, 2 * P.kblocks * TILE_BYTES);
+        else mbar_arrive_remote(afull, 0);
+      } else if (!TS) {
         mbar_expect_tx(afull, P.kblocks * TILE_BYTES);
         for (uint32_t kb = 0; kb < P.kblocks; ++kb)
           tma_load_2d(smem_u32(sA + kb * TILE_BYTES), &tmA, afull, kb * TC_BK, row0);
@@ -253,20 +343,28 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (uint32_t kb = 0; kb < P.kblocks; ++kb, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(empty0 + 8 * s, ph ^ 1);
-          mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
-          tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
-                      tile_of(t) * TC_BN);
+          if (PAIR) {
+            // this CTA's half of the tile: points [tile*128 + rank*64, +64)
+            tma_load_2d_pair(smem_u32(sB + s * BTILE), &tmB, full0 + 8 * s, kb * TC_BK,
+                             tile_of(t) * TC_BN + rank * (TC_BN / 2));
+            if (leader) mbar_expect_tx(full0 + 8 * s, 2 * BTILE);
+            else mbar_arrive_remote(full0 + 8 * s, 0);
+          } else {
+            mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
+            tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
+                        tile_of(t) * TC_BN);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
-    if (lane == 0) {
+    // ---------------- MMA issuer (one thread; the leader's, for a pair)
+    if (lane == 0 && leader) {
       mbar_wait(afull, 0);
       tc_fence_after();
       uint32_t it = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
-        const uint32_t acc = t % TC_ACC, aph = (t / TC_ACC) & 1;
+        const uint32_t acc = t % ACC, aph = (t / ACC) & 1;
         mbar_wait(tempty0 + 8 * acc, aph ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem + acc * TC_BN;
@@ -274,21 +372,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
-          const uint64_t bd = sw128_desc(smem_u32(sB + s * TILE_BYTES));
-#if CAGRA_KNN_TS
+          const uint64_t bd = sw128_desc(smem_u32(sB + s * BTILE));
+          if (TS) {
 #pragma unroll
-          for (uint32_t k = 0; k < TC_BK / 16; ++k)  // A: 16 bf16 = 8 TMEM columns per step
-            tc_mma_ts(dcol, tmem + TC_A_COL + kb * (TC_BK / 2) + k * 8, bd + 2 * k, kIdesc,
-                      (kb | k) != 0);
-#else
-          const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
+            for (uint32_t k = 0; k < TC_BK / 16; ++k)  // A: 16 bf16 = 8 TMEM columns per step
+              tc_mma_ts(dcol, tmem + TC_A_COL + kb * (TC_BK / 2) + k * 8, bd + 2 * k, idesc,
+                        (kb | k) != 0);
+          } else {
+            const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
 #pragma unroll
-          for (uint32_t k = 0; k < TC_BK / 16; ++k)  // 16 bf16 = 32 B = +2 in the address field
-            tc_mma(dcol, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0);
-#endif
-          tc_commit(empty0 + 8 * s);
+            for (uint32_t k = 0; k < TC_BK / 16; ++k) {  // 16 bf16 = 32 B = +2 in the address
+              if (PAIR) tc_mma_pair(dcol, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              else tc_mma(dcol, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            }
+          }
+          if (PAIR) tc_commit_pair(empty0 + 8 * s);
+          else tc_commit(empty0 + 8 * s);
         }
-        tc_commit(tfull0 + 8 * acc);
+        if (PAIR) tc_commit_pair(tfull0 + 8 * acc);
+        else tc_commit(tfull0 + 8 * acc);
       }
     }
   } else {
@@ -297,8 +399,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t rl = q4 * 32 + lane;         // row within the tile
     const uint32_t row = row0 + rl;
     const bool live = row < P.nq;
-#if CAGRA_KNN_TS
-    {
+    uint64_t* mypend = pend;
+    const uint32_t c_lo = 0, c_hi = TC_BN / 32;
+    if (TS) {
       // this row of A -> TMEM lane rl, columns [TC_A_COL, TC_A_COL + Kp/2)
       const uint32_t half = P.kblocks * (TC_BK / 2);
       const uint32_t* src = P.prow + (size_t)(live ? row : 0) * half;
@@ -310,9 +413,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(afull);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(afull);
     }
-#endif
     if (P.mode == 0) {
       for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
         const uint32_t rr = row0 + q4 * 32 + r;
@@ -332,15 +435,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 ? self_id / P.col_stride
                                 : 0xffffffffu;
     // append mode: copy every lane's pending keys to its row's global buffer
+    // (this lane owns the row: a register count, no atomics; a final count
+    // above capg marks an overflowed row for the fallback)
     auto spill = [&]() {
       if (live && cnt) {
-        if (gcnt + cnt <= P.capg) {
-          uint64_t* b = P.bufs + (size_t)row * P.capg + gcnt;
-          for (uint32_t i = 0; i < cnt; ++i) b[i] = pend[i * TC_BM + rl];
-          gcnt += cnt;
-        } else {
-          gcnt = P.capg + 1;  // overflow: the row is redone by the fallback
-        }
+        uint64_t* b = P.bufs + (size_t)row * P.capg;
+        for (uint32_t i = 0; i < cnt && gcnt + i < P.capg; ++i)
+          b[gcnt + i] = mypend[i * TC_BM + rl];
+        gcnt += cnt;
       }
       cnt = 0;
       __syncwarp();
@@ -400,17 +502,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       __syncwarp();
     };
     for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t acc = t % TC_ACC, aph = (t / TC_ACC) & 1;
+      const uint32_t acc = t % ACC, aph = (t / ACC) & 1;
       mbar_wait(tfull0 + 8 * acc, aph);
       tc_fence_after();
 #pragma unroll 1
-      for (uint32_t c = 0; c < TC_BN / 32; ++c) {
+      for (uint32_t c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
         tmem_ld32_nowait(tmem + ((q4 * 32) << 16) + acc * TC_BN + c * 32, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == TC_BN / 32 - 1) {
+        if (c == c_hi - 1) {
+          // release the accumulator: one arrival per warp, at the leader for a pair
           tc_fence_before();
-          mbar_arrive(tempty0 + 8 * acc);
+          __syncwarp();
+          if (lane == 0) {
+            if (PAIR) mbar_arrive_remote(tempty0 + 8 * acc, 0);
+            else mbar_arrive(tempty0 + 8 * acc);
+          }
         }
         // fast path: the chunk's minimum against the threshold (FMNMX3 tree)
         float m3[11];
@@ -445,7 +552,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const float d = __uint_as_float(v[i]);
             const uint32_t col = cbase + i;
             if (d <= tau_f && col < P.n && col != self_c) {
-              pend[cnt * TC_BM + rl] = make_key(fmaxf(d, 0.0f), col * P.col_stride);
+              mypend[cnt * TC_BM + rl] = make_key(fmaxf(d, 0.0f), col * P.col_stride);
               ++cnt;
             }
           };
@@ -475,10 +582,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       if (live) P.bcount[row] = gcnt;
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if (PAIR) cluster_sync_all();  // the peer's TMEM is written by the leader's MMAs
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -730,6 +842,8 @@ __global__ void scatter_rows_kernel(const uint32_t* __restrict__ rows, uint32_t 
 }
 
 // ------------------------------------------------------------ host side ----
+// Scratch of one kNN call.  (A stream-ordered pool was measured slower for
+// the first, cold build — the one a graph build pays — so plain cudaMalloc.)
 struct Dev {
   void* p = nullptr;
   explicit Dev(size_t b) { CAGRA_CUDA_TRY(cudaMalloc(&p, b ? b : 16)); }
@@ -761,12 +875,14 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// rows x Kp bf16, consecutive rows `row_step` rows apart in memory
-CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_step) {
+// rows x Kp bf16, consecutive rows `row_step` rows apart in memory; boxes of
+// 64 bf16 x box_rows rows
+CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_step,
+                     uint32_t box_rows = TC_BN) {
   CUtensorMap tm;
   cuuint64_t dims[2] = {Kp, rows};
   cuuint64_t strides[1] = {(cuuint64_t)Kp * 2 * row_step};
-  cuuint32_t box[2] = {TC_BK, TC_BN};
+  cuuint32_t box[2] = {TC_BK, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -776,17 +892,20 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_
   return tm;
 }
 
-size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_PEND) {
-  return 1024 + (CAGRA_KNN_TS ? 0 : (size_t)kblocks * TILE_BYTES) + stages * TILE_BYTES +
-         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * TC_ACC) + 16;
+size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_PEND,
+                     bool pair = false) {
+  const bool ts = CAGRA_KNN_TS && !pair;
+  const size_t btile = pair ? TILE_BYTES / 2 : TILE_BYTES;
+  return 1024 + (ts ? 0 : (size_t)kblocks * TILE_BYTES) + stages * btile +
+         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * (ts ? 2 : 4)) + 16;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
 // deepest B ring that fits next to the resident query tile
-uint32_t tc_stages(uint32_t kblocks, uint32_t pend_cap = TC_PEND) {
-  uint32_t s = TC_STAGES;
-  while (s > 2 && tc_smem_bytes(kblocks, s, pend_cap) > kSmemLimit) --s;
+uint32_t tc_stages(uint32_t kblocks, uint32_t pend_cap = TC_PEND, bool pair = false) {
+  uint32_t s = pair ? 2 * TC_STAGES : TC_STAGES;  // pair stages hold half tiles
+  while (s > 2 && tc_smem_bytes(kblocks, s, pend_cap, pair) > kSmemLimit) --s;
   return s;
 }
 
@@ -798,7 +917,8 @@ bool knn_tc_eligible(uint32_t dim, uint32_t K) {
   const char* env = std::getenv("CAGRA_KNN_PATH");
   if (env && std::strcmp(env, "simt") == 0) return false;
   uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK);
-  return Kp / TC_BK <= TC_MAX_KB && tc_smem_bytes(Kp / TC_BK, tc_stages(Kp / TC_BK)) <= kSmemLimit &&
+  return Kp / TC_BK <= TC_MAX_KB &&
+         tc_smem_bytes(Kp / TC_BK, tc_stages(Kp / TC_BK, TC_PEND, true), TC_PEND, true) <= kSmemLimit &&
          K + 32 + TC_PEND <= 256;
 }
 
@@ -815,21 +935,46 @@ struct TcCall {
   cudaStream_t stream;
 };
 
+// CTA pairs (cluster of 2, cta_group::2 MMA) with CAGRA_TC_PAIR=1.
+bool tc_pair_enabled() {
+  const char* e = std::getenv("CAGRA_TC_PAIR");  // measured slower than single CTAs: opt-in
+  return e && e[0] == '1';
+}
+
 void run_tc_kernel(const TcCall& c, const void* Pq, const CUtensorMap& tmA,
                    const CUtensorMap& tmB, TcArgs a, uint32_t nq) {
+  const bool pair = tc_pair_enabled();
   a.kblocks = c.kblocks;
   a.prow = reinterpret_cast<const uint32_t*>(Pq);
   const char* ge = std::getenv("CAGRA_TC_GROUPS");
   a.groups = ge ? (uint32_t)std::atoi(ge) : 1u;  // measured: the lockstep sweep wins (L2 reuse)
   a.pend_cap = a.mode == 1 ? TC_PEND_APPEND : TC_PEND;
-  a.stages = tc_stages(c.kblocks, a.pend_cap);
+  a.stages = tc_stages(c.kblocks, a.pend_cap, pair);
   a.exclude_self = c.exclude_self ? 1 : 0;
   a.nq = nq;
-  size_t smem = tc_smem_bytes(c.kblocks, a.stages, a.pend_cap);
-  CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  knn_tc_kernel<<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
-  CAGRA_LAUNCH_CHECK();
+  const size_t smem = tc_smem_bytes(c.kblocks, a.stages, a.pend_cap, pair);
+  if (!pair) {
+    CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    knn_tc_kernel<false><<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
+    CAGRA_LAUNCH_CHECK();
+    return;
+  }
+  CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * ((nq + 2 * TC_BM - 1) / (2 * TC_BM)));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CAGRA_CUDA_TRY(cudaLaunchKernelEx(&cfg, knn_tc_kernel<true>, tmA, tmB, a));
 }
 
 // Rows [0, nq) of the query side P (bf16, Kp wide; norms qnorm; fp32 rows
@@ -843,7 +988,8 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   Dev lists(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
   CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, c.stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, c.stream));
-  CUtensorMap tmA = make_map(P, nq, c.Kp, 1), tmB = make_map(c.R, c.n, c.Kp, 1);
+  const uint32_t brows = tc_pair_enabled() ? TC_BN / 2 : TC_BN;
+  CUtensorMap tmA = make_map(P, nq, c.Kp, 1), tmB = make_map(c.R, c.n, c.Kp, 1, brows);
   TcArgs a{};
   a.n = c.n;
   a.KC = KC;
@@ -953,9 +1099,11 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
         rer(8);
     CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, stream));
     CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(bcount.p, 0, 4ull * nq, stream));  // append counters
+    const uint32_t brows = tc_pair_enabled() ? TC_BN / 2 : TC_BN;
     CUtensorMap tmA = make_map(dP.p, nq, c.Kp, 1);
-    CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride);
-    CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1);
+    CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride, brows);
+    CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1, brows);
     TcArgs a{};
     a.n = ns;
     a.KC = r;

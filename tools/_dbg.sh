@@ -1,5 +1,5 @@
-python -c "import torch;print(torch.cuda.get_device_properties(0))" > gpurun_out/l2p.log 2>&1
-for f in none 0.5 0.75; do
-  if [ $f = none ]; then unset CAGRA_L2_PERSIST; else export CAGRA_L2_PERSIST=$f; fi
-  python tools/sweep.py --grid '896,16,1,12,0,1' 2>&1 | grep "M=" | sed "s/^/persist=$f /" >> gpurun_out/l2p.log
+for v in new prev new prev; do
+  if [ $v = new ]; then L=paper_2308_15136_b200/lib/libcagra_b200.so; else L=lib_variants/libcagra_prev.so; fi
+  CAGRA_LIB=$L timeout 120 python tools/knn_prof.py 1000000 2>&1 | sed "s/^/$v /" | cut -c1-100 >> gpurun_out/knn_ab3.log
 done
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "knn or gist or build or ground" -q 2>&1 | tail -1 >> gpurun_out/knn_ab3.log
