@@ -315,11 +315,13 @@ struct Smem {
   uint64_t* fin;       // shared mode: merged team results
 };
 
+constexpr int kSelChunks = 8;  // select_parents chunks per barrier round
+
 struct Ctl {
   uint32_t qi, nev, npar_total, count, dup, slow;
   uint32_t nsurv[16];
   uint32_t npar[16];
-  uint32_t warp_cnt[SWARPS];
+  uint32_t warp_cnt[kSelChunks * SWARPS];
   uint64_t worst[16];
   uint32_t iters[16];
   uint32_t done[16];
@@ -455,6 +457,16 @@ __device__ __forceinline__ void eval_list_generic(const KParams& P, const Smem& 
   }
 }
 
+// Clear of the shared-memory visited table: 16-byte stores (the table is
+// 16-byte aligned and hcap is a power of two >= 4 whenever it lives in smem).
+__device__ __forceinline__ void smem_table_clear(uint32_t* t, uint32_t hcap) {
+  const uint4 inv = make_uint4(kInvalidId, kInvalidId, kInvalidId, kInvalidId);
+  uint4* t4 = reinterpret_cast<uint4*>(t);
+  for (uint32_t i = threadIdx.x; i < (hcap >> 2); i += SNT) t4[i] = inv;
+  if (hcap < 4)
+    for (uint32_t i = threadIdx.x; i < hcap; i += SNT) t[i] = kInvalidId;
+}
+
 // Visited-table reset with the current top-M ids (reset_table,
 // search.cpp:138-145).  Called by all threads; top-M ids are distinct, so the
 // parallel inserts fill exactly the first min(live, hcap) entries.
@@ -462,7 +474,7 @@ template <bool SMEM_TABLE>
 __device__ void table_reset(const KParams& P, const Smem& S, Ctl& ctl, const uint64_t* top,
                             unsigned long long* gtab, uint32_t& tag) {
   if (SMEM_TABLE) {
-    for (uint32_t i = threadIdx.x; i < P.hcap; i += SNT) S.table[i] = kInvalidId;
+    smem_table_clear(S.table, P.hcap);
   } else {
     tag = tag + 1;  // every thread keeps the same register copy
   }
@@ -572,7 +584,7 @@ search_kernel(const KParams P) {
     S.surv = reinterpret_cast<uint64_t*>(p);
     p += sizeof(uint64_t) * SP;
     S.evlist = reinterpret_cast<uint32_t*>(p);
-    p += sizeof(uint32_t) * P.C;
+    p += sizeof(uint32_t) * round_up_u32(P.C, 4);  // keeps the table 16-byte aligned
     S.evteam = nullptr;  // one team: every candidate belongs to team 0
     S.parents = reinterpret_cast<uint32_t*>(p);
     p += sizeof(uint32_t) * round_up_u32(P.p, 4);
@@ -592,8 +604,7 @@ search_kernel(const KParams P) {
     const uint32_t qreal = P.mc_teams ? qi / P.mc_teams : qi;
     for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qreal * P.ld + i];
     for (uint32_t i = tid; i < P.M; i += SNT) S.topA[i] = kDummyKey;
-    if (SMEM_TABLE)
-      for (uint32_t i = tid; i < P.hcap; i += SNT) S.table[i] = kInvalidId;
+    if (SMEM_TABLE) smem_table_clear(S.table, P.hcap);
     if (!SMEM_TABLE && P.mc_teams) {
       gtab = P.gtables + (size_t)qreal * P.hcap;  // shared by the query's teams
       tag = P.mc_tag;
@@ -806,34 +817,43 @@ search_kernel(const KParams P) {
       PROF_T(ts0);
       pending = false;
       ++iters;
-      // select_parents: first p unflagged non-dummy entries
-      if (tid == 0) ctl.npar[0] = 0;
-      __syncthreads();
-      for (uint32_t c0 = 0; c0 < P.M; c0 += SNT) {
-        uint32_t have = ctl.npar[0];
-        if (have >= P.p) break;
-        uint32_t i = c0 + tid;
-        uint64_t e = i < P.M ? top[i] : kDummyKey;
-        bool elig = i < P.M && !key_is_dummy(e) && !(e & kFlagBit64);
-        unsigned bal = __ballot_sync(0xffffffffu, elig);
-        if (lane == 0) ctl.warp_cnt[warp] = __popc(bal);
-        __syncthreads();
-        uint32_t off = 0, tot = 0;
-        for (int w = 0; w < SWARPS; ++w) {
-          uint32_t c = ctl.warp_cnt[w];
-          if (w < warp) off += c;
-          tot += c;
-        }
-        uint32_t rank = have + off + __popc(bal & ((1u << lane) - 1));
-        if (elig && rank < P.p) {
-          S.parents[rank] = key_id(e) & kIdMask;
-          top[i] = e | kFlagBit64;
+      // select_parents: first p unflagged non-dummy entries.  Up to 8 chunks
+      // of SNT entries per round: one barrier publishes every warp's count of
+      // eligible entries, then each thread ranks its entries in list order.
+      uint32_t np = 0;
+      for (uint32_t g0 = 0; g0 < P.M && np < P.p; g0 += kSelChunks * SNT) {
+        const uint32_t nch = min((uint32_t)kSelChunks, (P.M - g0 + SNT - 1) / SNT);
+        for (uint32_t c = 0; c < nch; ++c) {
+          uint32_t i = g0 + c * SNT + tid;
+          uint64_t e = i < P.M ? top[i] : kDummyKey;
+          bool elig = i < P.M && !key_is_dummy(e) && !(e & kFlagBit64);
+          unsigned bal = __ballot_sync(0xffffffffu, elig);
+          if (lane == 0) ctl.warp_cnt[c * SWARPS + warp] = __popc(bal);
         }
         __syncthreads();
-        if (tid == 0) ctl.npar[0] = min(P.p, have + tot);
+        uint32_t run = np;
+        for (uint32_t c = 0; c < nch && run < P.p; ++c) {
+          uint32_t i = g0 + c * SNT + tid;
+          uint64_t e = i < P.M ? top[i] : kDummyKey;
+          bool elig = i < P.M && !key_is_dummy(e) && !(e & kFlagBit64);
+          unsigned bal = __ballot_sync(0xffffffffu, elig);
+          uint32_t off = 0, tot = 0;
+#pragma unroll
+          for (int w = 0; w < SWARPS; ++w) {
+            uint32_t cw = ctl.warp_cnt[c * SWARPS + w];
+            off += w < warp ? cw : 0u;
+            tot += cw;
+          }
+          uint32_t rank = run + off + __popc(bal & ((1u << lane) - 1));
+          if (elig && rank < P.p) {
+            S.parents[rank] = key_id(e) & kIdMask;
+            top[i] = e | kFlagBit64;
+          }
+          run += tot;
+        }
+        np = min(P.p, run);
         __syncthreads();
       }
-      uint32_t np = ctl.npar[0];
       PROF_ADD(3, ts0);
       DBG("q%u it%u np=%u\n", qi, iters, np);
       if (np == 0) {
@@ -1385,7 +1405,7 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   size_t smem;
   if (!shared) {
     uint32_t SP = std::max(256u, next_pow2_u32(C));
-    smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * C + 4ull * round_up_u32(p, 4) +
+    smem = 4ull * ldr + 16ull * c.topm + 8ull * SP + 4ull * round_up_u32(C, 4) + 4ull * round_up_u32(p, 4) +
            (pl.smem_table ? 4ull * hcap : 0);
   } else {
     if (d > 256) throw UsageErr("batch_search: shared mode on device needs graph degree <= 256");
