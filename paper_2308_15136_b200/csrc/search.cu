@@ -86,9 +86,20 @@ struct KParams {
   DevStats* team_stats;          // [nq * teams]
 };
 
+// Phase profiler: compiled in only with -DCAGRA_PROF_BUILD (tools/build_variant.sh),
+// then enabled at run time by CAGRA_SEARCH_PROF=1.  The production build has
+// no timestamps live across phases (64-register budget of the search kernel).
+#ifdef CAGRA_PROF_BUILD
 #define PROF_T(var) long long var = (P.prof && threadIdx.x == 0) ? clock64() : 0
 #define PROF_ADD(slot, since) \
   do { if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[slot], (unsigned long long)(clock64() - since)); } while (0)
+#define PROF_CNT(slot, v) \
+  do { if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[slot], (unsigned long long)(v)); } while (0)
+#else
+#define PROF_T(var)
+#define PROF_ADD(slot, since) do { } while (0)
+#define PROF_CNT(slot, v) do { } while (0)
+#endif
 
 // ------------------------------------------------------------- init ids ----
 __global__ void init_samples_kernel(uint32_t nq, uint32_t C, uint32_t teams, uint32_t n,
@@ -316,6 +327,7 @@ struct Smem {
 };
 
 constexpr int kSelChunks = 8;  // select_parents chunks per barrier round
+
 
 struct Ctl {
   uint32_t qi, nev, npar_total, count, dup, slow;
@@ -728,15 +740,25 @@ search_kernel(const KParams P) {
     auto merge = [&]() {
       uint32_t ns = ctl.nsurv[0];
       if (ns > 0) {
+        PROF_T(tq0);
+        PROF_CNT(8, ns);
+        PROF_CNT(9, 1);
         // drop duplicates of top-M entries (forgettable revisits)
         if (forget) {
           for (uint32_t j = tid; j < ns; j += SNT) {
             uint64_t s = S.surv[j];
             uint32_t ix = lb_cmp(top, P.M, s);
-            if (ix < P.M && cmp_key(top[ix]) == s) S.surv[j] = kDummyKey;
+            if (ix < P.M && cmp_key(top[ix]) == s) {
+              S.surv[j] = kDummyKey;
+#ifdef CAGRA_PROF_BUILD
+              if (P.prof) atomicAdd(&P.prof[10], 1ull);
+#endif
+            }
           }
           __syncthreads();
         }
+        PROF_ADD(5, tq0);
+        PROF_T(tq1);
         if (ns <= 64) {
           if (warp == 0) warp_sort_smem(S.surv, ns, lane);
         } else {
@@ -772,6 +794,8 @@ search_kernel(const KParams P) {
           }
           ns = lo;
         }
+        PROF_ADD(6, tq1);
+        PROF_T(tq2);
         for (uint32_t i = tid; i < P.M; i += SNT) {
           uint64_t e = top[i];
           uint32_t lo = 0, hi = ns;
@@ -790,6 +814,7 @@ search_kernel(const KParams P) {
           if (pos < P.M) nxt[pos] = s;
         }
         __syncthreads();
+        PROF_ADD(7, tq2);
         uint64_t* t = top;
         top = nxt;
         nxt = t;
@@ -1511,11 +1536,15 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.stats = reinterpret_cast<DevStats*>(d_stats);
   P.error = nullptr;
   P.prof = nullptr;
+#ifdef CAGRA_PROF_BUILD
   const char* penv = std::getenv("CAGRA_SEARCH_PROF");
+#else
+  const char* penv = nullptr;  // phase profiler not compiled in
+#endif
   static unsigned long long* d_prof = nullptr;
   if (penv && penv[0] == '1') {
-    if (!d_prof) CAGRA_CUDA_TRY(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
-    CAGRA_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), stream));
+    if (!d_prof) CAGRA_CUDA_TRY(cudaMalloc(&d_prof, 16 * sizeof(unsigned long long)));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), stream));
     P.prof = d_prof;
   }
   KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(pl.fn));
@@ -1535,7 +1564,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
     ++launches;
   }
   if (P.prof) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     CAGRA_CUDA_TRY(cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
     CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
     double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
@@ -1544,6 +1573,10 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
             pl.grid, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4],
             100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot,
             100 * h[4] / tot);
+    if (h[9])
+      fprintf(stderr, "search prof merge: dedup %.3g sort %.3g place %.3g | merges %llu "
+                      "mean survivors %.1f dups %llu\n",
+              (double)h[5], (double)h[6], (double)h[7], h[9], (double)h[8] / h[9], h[10]);
   }
   return launches;
 }

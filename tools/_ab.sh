@@ -1,7 +1,9 @@
-# A/B of two libcagra builds on one box: ablib/libcagra_old.so vs the in-tree build.
-set -x
+# A/B of libcagra builds on one box: ablib/libcagra_<name>.so for each name in
+# $AB_LIBS (default "old"), interleaved with the in-tree build ("new"), $AB_REPS rounds.
 G=${AB_GRID:-896,16,1,12,0,1}
-for r in 1 2 3; do
-  CAGRA_LIB=$PWD/ablib/libcagra_old.so timeout 300 python tools/sweep.py --grid "$G" 2>&1 | tail -1 | sed 's/^/OLD /'
-  timeout 300 python tools/sweep.py --grid "$G" 2>&1 | tail -1 | sed 's/^/NEW /'
+for r in $(seq ${AB_REPS:-3}); do
+  for v in ${AB_LIBS:-old} new; do
+    if [ $v = new ]; then L=""; else L=$PWD/ablib/libcagra_$v.so; fi
+    CAGRA_LIB=$L timeout 300 python tools/sweep.py --grid "$G" 2>&1 | tail -1 | sed "s/^/$v /"
+  done
 done
