@@ -264,6 +264,15 @@ __device__ __forceinline__ uint32_t warp_append_slot(uint32_t* ctr, bool pred) {
 
 // ------------------------------------------------------------ visited -----
 // Shared-memory table: u32 slots, kInvalidId = empty.
+__device__ __forceinline__ bool smem_insert_from(uint32_t* tab, uint32_t mask, uint32_t id,
+                                                 uint32_t h) {
+  for (;;) {
+    uint32_t old = atomicCAS(&tab[h], kInvalidId, id);
+    if (old == kInvalidId) return true;
+    if (old == id) return false;
+    h = (h + 1) & mask;
+  }
+}
 __device__ __forceinline__ bool smem_insert(uint32_t* tab, uint32_t mask, uint32_t id) {
   uint32_t h = hash_id(id, mask);
   for (;;) {
@@ -330,7 +339,7 @@ constexpr int kSelChunks = 8;  // select_parents chunks per barrier round
 
 
 struct Ctl {
-  uint32_t qi, nev, npar_total, count, dup, slow;
+  uint32_t qi, nev, npar_total, count, dup, slow, nfresh;
   uint32_t nsurv[16];
   uint32_t npar[16];
   uint32_t warp_cnt[kSelChunks * SWARPS];
@@ -343,9 +352,14 @@ struct Ctl {
   uint32_t pending[16];
 };
 
-template <int TEAM, int MAXC, bool EXACT>
+// SPEC (multi-CTA mode): the candidates were not filtered by the visited
+// table; the team leader issues the table insert right after the row loads,
+// so the atomic's L2 round trip overlaps the row gather, and only first
+// visits are kept and counted (ctl.nfresh).
+template <int TEAM, int MAXC, bool EXACT, bool SPEC = false>
 __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& ctl,
-                                          uint32_t nev, uint32_t SP) {
+                                          uint32_t nev, uint32_t SP,
+                                          uint32_t* spec_tab = nullptr, uint32_t spec_mask = 0) {
   const int tid = threadIdx.x;
   if (EXACT) {
     for (uint32_t e0 = 0; e0 < nev; e0 += SNT) {
@@ -398,6 +412,26 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
           xv[u][c] = (e < nev && ch < nchunk) ? __ldg(row + ch) : make_float4(0, 0, 0, 0);
         }
       }
+      uint32_t fresh = 0;  // SPEC: bit u = first visit of candidate u
+      if (SPEC && lt == 0) {
+        uint32_t old[U], h[U], ids[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // first probes of all U inserts in flight together
+          uint32_t e = e0 + u * NTEAMS;
+          ids[u] = e < nev ? S.evlist[e] : kInvalidId;
+          h[u] = hash_id(ids[u], spec_mask);
+          old[u] = e < nev ? atomicCAS(&spec_tab[h[u]], kInvalidId, ids[u]) : ids[u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bool ins = old[u] == kInvalidId;
+          if (!ins && old[u] != ids[u])  // collision: continue the linear probe
+            ins = smem_insert_from(spec_tab, spec_mask, ids[u], (h[u] + 1) & spec_mask);
+          fresh |= (ins ? 1u : 0u) << u;
+        }
+        const uint32_t nf = __popc(fresh);
+        if (nf) atomicAdd(&ctl.nfresh, nf);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         float acc = 0.0f;
@@ -420,7 +454,7 @@ __device__ __forceinline__ void eval_list(const KParams& P, const Smem& S, Ctl& 
           uint32_t id = S.evlist[e];
           t = P.teams == 1 ? 0u : S.evteam[e];
           key = make_key(acc, id);
-          keep = key < ctl.worst[t];
+          keep = key < ctl.worst[t] && (!SPEC || ((fresh >> u) & 1u));
         }
         if (P.teams == 1) {
           const uint32_t pos = warp_append_slot(&ctl.nsurv[0], keep);
@@ -577,7 +611,9 @@ __device__ void serial_visit(const KParams& P, const Smem& S, Ctl& ctl, const ui
 #ifndef CAGRA_SEARCH_MINB
 #define CAGRA_SEARCH_MINB 4  // 64 registers: 4 CTAs (1024 threads) per SM; the heuristic alone is unstable
 #endif
-template <int TEAM, int MAXC, bool EXACT, bool SMEM_TABLE>
+// MC: multi-CTA instantiation (P.mc_teams > 0, shared HBM visited table):
+// graph candidates go to eval unfiltered and are inserted there (SPEC above).
+template <int TEAM, int MAXC, bool EXACT, bool SMEM_TABLE, bool MC = false>
 __global__ void __launch_bounds__(SNT, CAGRA_SEARCH_MINB)
 search_kernel(const KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -663,7 +699,19 @@ search_kernel(const KParams P) {
     auto visit = [&](const uint32_t* src_ids, bool from_graph, uint32_t cnt) {
       PROF_T(tv0);
       bool slow = forget && (ctl.count + cnt > P.hcap);
-      if (!slow) {
+      if (MC && MAXC > 0 && from_graph) {
+        for (uint32_t j = tid; j < cnt; j += SNT) {
+          const uint32_t pi = j >> P.deg_shift, c = j & (P.degree - 1);
+          S.evlist[j] = P.deg_shift != 0xffu
+                            ? __ldg(&P.graph[(size_t)S.parents[pi] * P.degree + c])
+                            : __ldg(&P.graph[(size_t)S.parents[j / P.degree] * P.degree +
+                                             j % P.degree]);
+        }
+        if (tid == 0) {
+          ctl.nev = cnt;
+          ctl.nfresh = 0;
+        }
+      } else if (!slow) {
         if (tid == 0) ctl.nev = 0;
         __syncthreads();
         // all of this thread's candidate ids are loaded before any insert, so
@@ -729,9 +777,19 @@ search_kernel(const KParams P) {
       PROF_ADD(0, tv0);
       PROF_T(te0);
       uint32_t nev = ctl.nev;
-      if (MAXC > 0) eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT>(P, S, ctl, nev, SP);
-      else eval_list_generic<EXACT>(P, S, ctl, nev, SP);
-      if (tid == 0) ctl.evals[0] += nev;
+      if (MC && MAXC > 0 && from_graph) {
+        eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT, true>(
+            P, S, ctl, nev, SP, P.mc_tab + (size_t)qreal * P.hcap, mask);
+        __syncthreads();
+        if (tid == 0) {
+          ctl.evals[0] += ctl.nfresh;
+          ctl.count += ctl.nfresh;
+        }
+      } else {
+        if (MAXC > 0) eval_list<TEAM, (MAXC > 0 ? MAXC : 1), EXACT>(P, S, ctl, nev, SP);
+        else eval_list_generic<EXACT>(P, S, ctl, nev, SP);
+        if (tid == 0) ctl.evals[0] += nev;
+      }
       __syncthreads();
       PROF_ADD(1, te0);
     };
@@ -1363,6 +1421,18 @@ Variant pick_variant(uint32_t ld, uint32_t req_team) {
 
 using KernelFn = void (*)(const KParams);
 
+// multi-CTA mode (fast distances only): speculative-insert instantiation
+KernelFn mc_fn(Variant v) {
+  switch (v.team * 100 + v.maxc) {
+    case 402: return search_kernel<4, 2, false, false, true>;
+    case 803: return search_kernel<8, 3, false, false, true>;
+    case 804: return search_kernel<8, 4, false, false, true>;
+    case 1604: return search_kernel<16, 4, false, false, true>;
+    case 3208: return search_kernel<32, 8, false, false, true>;
+    default: return search_kernel<32, 0, false, false>;
+  }
+}
+
 template <bool EXACT, bool SMEM>
 KernelFn per_query_fn(Variant v) {
   if (EXACT) return search_kernel<32, 1, true, SMEM>;
@@ -1442,11 +1512,11 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
     throw UsageErr("search: parameters exceed the device shared-memory budget");
   pl.smem = smem;
   Variant v = pick_variant(ix.ld, c.team_size);
-  KernelFn fn = shared ? shared_fn(c.exact != 0, v)
-                       : (pl.smem_table ? (c.exact ? per_query_fn<true, true>(v)
-                                                   : per_query_fn<false, true>(v))
-                                        : (c.exact ? per_query_fn<true, false>(v)
-                                                   : per_query_fn<false, false>(v)));
+  KernelFn fn;
+  if (shared) fn = shared_fn(c.exact != 0, v);
+  else if (pl.mc) fn = mc_fn(v);
+  else if (pl.smem_table) fn = c.exact ? per_query_fn<true, true>(v) : per_query_fn<false, true>(v);
+  else fn = c.exact ? per_query_fn<true, false>(v) : per_query_fn<false, false>(v);
   pl.fn = reinterpret_cast<const void*>(fn);
   CAGRA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
