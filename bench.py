@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--b1-topm", type=int, default=16, help="batch-1 team top-M")
     ap.add_argument("--b1-teams", type=int, default=64, help="batch-1 teams (one CTA each)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--build-once", action="store_true",
+                    help="one graph build (large configs): graph_build_s is then the first build")
     return ap.parse_args()
 
 
@@ -286,10 +288,12 @@ def run_ours(args):
     # the driver mapping ~2 GB of fresh device memory): reported as
     # first_build_s; the graph_build_s figures are the steady-state second build.
     t0 = time.perf_counter()
-    _, binfo0 = fodg.build_graph(ds, args.degree, device=local)
-    first_build = {"knn": binfo0["knn_seconds"], "wall": time.perf_counter() - t0}
-    t0 = time.perf_counter()
     g, binfo = fodg.build_graph(ds, args.degree, device=local)
+    first_build = {"knn": binfo["knn_seconds"], "wall": time.perf_counter() - t0}
+    if not args.build_once:
+        del g
+        t0 = time.perf_counter()
+        g, binfo = fodg.build_graph(ds, args.degree, device=local)
     build_wall = time.perf_counter() - t0
     kst = capi.knn_last_stats()
     kp = -(-(3 * args.dim + 6) // 64) * 64
