@@ -300,8 +300,10 @@ def run_ours(args):
     # bf16 tensor-core work of the kNN build: sample pass (1/16) + full pass,
     # 2*N*N*Kp each (Kp = 3*dim + 6 padded to 64: bf16x3 split + folded norms)
     tc_flops = 2.0 * args.n * args.n * kp * (1 + 1 / 16)
-    knn_stats = {"path": "tcgen05 bf16x3 GEMM + exact re-rank (bit-exact)",
-                 "tensor_tflops": tc_flops / binfo["knn_seconds"] / 1e12,
+    tc = kst["rows"] > 0  # 0 rows: the SIMT sequential-chain kernel ran (dim too large)
+    knn_stats = {"path": ("tcgen05 bf16x3 GEMM + exact re-rank (bit-exact)" if tc else
+                          "SIMT sequential-chain fp32 (bit-exact; dim beyond the tensor-core path)"),
+                 "tensor_tflops": tc_flops / binfo["knn_seconds"] / 1e12 if tc else None,
                  "fp32_equiv_tflops": 2.0 * args.n * args.n * args.dim / binfo["knn_seconds"] / 1e12,
                  "rows": kst["rows"], "fallback_rows": kst["fallback_rows"],
                  "retried_rows": kst["retried_rows"],

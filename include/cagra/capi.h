@@ -147,6 +147,14 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
 int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked,
                          uint64_t* retried_rows);
 
+/* ---- graph quality metrics ----------------------------------------------- */
+/* strong_cc_count (graph_metrics.hpp:22) and the integer total behind
+ * avg_2hop_count (graph_metrics.hpp:26; mean = two_hop_total / n), on the
+ * device.  graph: n x degree host ids (< n, else USAGE).  Either output may be
+ * NULL to skip that metric. */
+int cagra_graph_metrics(const uint32_t* graph, uint32_t n, uint32_t degree, int device,
+                        uint64_t* strong_cc, uint64_t* two_hop_total);
+
 /* ---- graph optimization (rank mode) -------------------------------------- */
 /* count_detourable_routes (graph_opt.hpp:47-49), rank mode.  Rejects rows not
  * sorted by (dist, id) with USAGE (graph_opt.cpp:19-31). */

@@ -214,6 +214,15 @@ class Reference(_Lib):
                                      C.c_uint32(int(add_reverse)), _p(out), _p(secs)))
         return out, secs
 
+    def graph_metrics(self, graph):
+        """(strong_cc_count, avg_2hop_count) of an n x d uint32 graph."""
+        n, d = graph.shape
+        scc = C.c_uint64(0)
+        avg = C.c_double(0)
+        _check(self.lib.ref_graph_metrics(_p(graph), C.c_uint32(n), C.c_uint32(d),
+                                          C.byref(scc), C.byref(avg)))
+        return int(scc.value), float(avg.value)
+
     def index(self, data, graph):
         return RefIndex(self, data, graph)
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "fodg/engine.hpp"
+#include "fodg/graph_metrics.hpp"
 #include "fodg/graph_opt.hpp"
 #include "fodg/knn_build.hpp"
 #include "fodg/search.hpp"
@@ -150,6 +151,19 @@ int ref_build_reverse_graph(const uint32_t* pruned, uint32_t n, uint32_t d, uint
       rev_counts[y] = (uint32_t)rg.rows[y].size();
       for (size_t j = 0; j < rg.rows[y].size(); ++j) rev_ids[(size_t)y * cap + j] = rg.rows[y][j];
     }
+  });
+}
+
+// strong_cc_count / avg_2hop_count (graph_metrics.hpp:22-26), num_threads 0
+int ref_graph_metrics(const uint32_t* graph, uint32_t n, uint32_t d, uint64_t* scc,
+                      double* avg_2hop) {
+  return guard([&] {
+    Graph g;
+    g.num_nodes = n;
+    g.degree = d;
+    g.ids.assign(graph, graph + (size_t)n * d);
+    *scc = strong_cc_count(g);
+    *avg_2hop = avg_2hop_count(g, 0);
   });
 }
 

@@ -88,6 +88,7 @@ EXPORTS = [
     "cagra_optimize", "cagra_build_graph", "cagra_index_create", "cagra_index_create_dev",
     "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
     "cagra_search_dev", "cagra_last_launch_count", "cagra_merge_shard_topk_dev",
+    "cagra_graph_metrics",
 ]
 
 _lib = None
@@ -112,6 +113,7 @@ def lib() -> C.CDLL:
         L.cagra_exact_topk.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp]
         L.cagra_knn_last_stats.argtypes = [vp, vp, vp, vp]
         L.cagra_count_detourable_routes.argtypes = [vp, vp, u32, u32, i32, vp]
+        L.cagra_graph_metrics.argtypes = [vp, u32, u32, i32, vp, vp]
         L.cagra_count_detourable_routes_distance.argtypes = [vp, vp, u32, u32, vp, u32, u32, i32,
                                                              vp]
         L.cagra_reorder_and_prune.argtypes = [vp, vp, u32, u32, u32, i32, vp]
@@ -162,6 +164,17 @@ def knn_last_stats() -> dict:
     v = (C.c_uint64 * 4)()
     lib().cagra_knn_last_stats(C.byref(v, 0), C.byref(v, 8), C.byref(v, 16), C.byref(v, 24))
     return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2], "retried_rows": v[3]}
+
+
+def graph_metrics(graph: np.ndarray, device: int = 0):
+    """(strong-CC count, distinct <=2-hop total) of an n x d uint32 graph,
+    computed on the device (cagra_graph_metrics)."""
+    g = np.ascontiguousarray(graph, np.uint32)
+    n, d = g.shape
+    scc = C.c_uint64(0)
+    tot = C.c_uint64(0)
+    check(lib().cagra_graph_metrics(ptr(g), n, d, device, C.byref(scc), C.byref(tot)))
+    return int(scc.value), int(tot.value)
 
 
 def mix_seed(x: int) -> int:

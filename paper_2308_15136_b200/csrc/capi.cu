@@ -554,6 +554,28 @@ int cagra_build_reverse_graph(const uint32_t* pruned, uint32_t n, uint32_t d, ui
   });
 }
 
+int cagra_graph_metrics(const uint32_t* graph, uint32_t n, uint32_t degree, int device,
+                        uint64_t* strong_cc, uint64_t* two_hop) {
+  return guarded([&] {
+    if (strong_cc) *strong_cc = 0;
+    if (two_hop) *two_hop = 0;
+    if (n == 0) return;
+    int dev = resolve_device(device);
+    DeviceScope scope(dev);
+    Stream st;
+    const size_t e = (size_t)n * degree;
+    DBuf dg(4 * e), flag(sizeof(int));
+    if (e) CAGRA_CUDA_TRY(cudaMemcpyAsync(dg.p, graph, 4 * e, cudaMemcpyHostToDevice, st.s));
+    CAGRA_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st.s));
+    if (e) launch_check_ids(dg.as<uint32_t>(), e, n, flag.as<int>(), st.s);
+    int h = 0;
+    read_flag(flag.as<int>(), &h, st.s);
+    if (h & 2) throw UsageErr("graph_metrics: neighbour id out of range");
+    if (strong_cc) *strong_cc = scc_count(dg.as<uint32_t>(), n, degree, st.s);
+    if (two_hop) *two_hop = two_hop_total(dg.as<uint32_t>(), n, degree, sm_count_of(dev), st.s);
+  });
+}
+
 int cagra_merge_graphs(const uint32_t* pruned, const uint32_t* rev_counts,
                        const uint32_t* rev_ids, uint32_t n, uint32_t d, uint32_t rev_cap,
                        int device, uint32_t* graph_out) {

@@ -33,6 +33,13 @@ struct KnnTcStats {
 };
 extern KnnTcStats g_knn_tc_stats;
 
+// ---- metrics.cu ---------------------------------------------------------------
+// Distinct <=2-hop neighbours summed over all nodes (avg_2hop_count * n) and
+// the strongly connected component count; synchronous on `stream`.
+uint64_t two_hop_total(const uint32_t* d_graph, uint32_t n, uint32_t d, int sm_count,
+                       cudaStream_t stream);
+uint64_t scc_count(const uint32_t* d_graph, uint32_t n, uint32_t d, cudaStream_t stream);
+
 // ---- graph_opt.cu -----------------------------------------------------------
 struct OptTimes {
   float count_ms = 0, reorder_ms = 0, reverse_ms = 0, merge_ms = 0, total_ms = 0;

@@ -461,6 +461,40 @@ def build_graph(ds: Dataset, d: int, d_init: Optional[int] = None, device: int =
 
 
 # ------------------------------------------------------------------- search --
+@dataclass
+class GraphQualityReport:
+    """graph_metrics.hpp:10-19."""
+    num_nodes: int = 0
+    degree: int = 0
+    strong_cc: int = 0
+    avg_2hop: float = 0.0
+    max_2hop: int = 0
+
+    def report(self) -> str:
+        return (f"num_nodes={self.num_nodes}\ndegree={self.degree}\nstrong_cc={self.strong_cc}\n"
+                f"avg_2hop={self.avg_2hop:g}\nmax_2hop={self.max_2hop}\n")
+
+
+def strong_cc_count(g: Graph, device: int = 0) -> int:
+    """graph_metrics.hpp:22 (on the device: trimming + colouring)."""
+    return capi.graph_metrics(g.ids.reshape(g.num_nodes, g.degree), device)[0] if g.num_nodes else 0
+
+
+def avg_2hop_count(g: Graph, num_threads: int = 0, device: int = 0) -> float:
+    """graph_metrics.hpp:26: mean distinct <=2-hop neighbours (exact integer total / n)."""
+    if g.num_nodes == 0:
+        return 0.0
+    return capi.graph_metrics(g.ids.reshape(g.num_nodes, g.degree), device)[1] / g.num_nodes
+
+
+def measure_graph(g: Graph, num_threads: int = 0, device: int = 0) -> GraphQualityReport:
+    """graph_metrics.hpp:28."""
+    scc, tot = (capi.graph_metrics(g.ids.reshape(g.num_nodes, g.degree), device)
+                if g.num_nodes else (0, 0))
+    return GraphQualityReport(g.num_nodes, g.degree, scc, tot / g.num_nodes if g.num_nodes else 0.0,
+                              g.degree * (1 + g.degree))
+
+
 class Index:
     """Device-resident (dataset, graph) — replaces the per-call `const Graph&,
     const Dataset&` of batch_search (engine.hpp:38-40)."""

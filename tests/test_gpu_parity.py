@@ -503,3 +503,36 @@ def test_search_empty_batch_and_limits(gpu, oracle):
     # dimension mismatch / graph-dataset mismatch, reference messages' classes
     with pytest.raises(fodg.UsageError):
         fodg.batch_search(g, ds, fodg.Dataset.from_array(data[:3, :4]), fodg.SearchParams())
+
+
+# ------------------------------------------------------- graph metrics ----
+def _metric_graphs(oracle):
+    rng = np.random.default_rng(5)
+    yield "functional d=1", rng.integers(0, 5000, (5000, 1), dtype=np.uint32)
+    yield "random d=3", rng.integers(0, 20000, (20000, 3), dtype=np.uint32)
+    chain = np.arange(-1, 999, dtype=np.int64).clip(0).astype(np.uint32).reshape(1000, 1)
+    yield "reverse chain + self loop", chain
+    yield "two-cycle", np.array([[1], [0]], np.uint32)
+    yield "dup ids in rows", rng.integers(0, 50, (300, 6), dtype=np.uint32)
+    data = oracle.uniform_dataset(2048, 32, 3)
+    ids, dists = oracle.exact_knn_graph(data, 48)
+    yield "optimized 2048x16", oracle.optimize(ids, dists, 16)
+    ds = fodg.Dataset.from_array(capi.uniform_dataset(100_000, 32, 424242))
+    g, _ = fodg.build_graph(ds, 32)
+    yield "optimized 100k x32", g.ids
+
+
+def test_graph_metrics_vs_reference(gpu, oracle, reference):
+    # graph_metrics.cpp:20-120: SCC count and the mean distinct 2-hop count,
+    # exact (integer total / n, same double)
+    for name, ids in _metric_graphs(oracle):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        n, d = ids.shape
+        g = fodg.Graph(n, d, ids)
+        want_scc, want_avg = reference.graph_metrics(ids)
+        rep = fodg.measure_graph(g)
+        assert rep.strong_cc == want_scc, name
+        assert rep.avg_2hop == want_avg, name
+        assert rep.max_2hop == d * (1 + d)
+    with pytest.raises(fodg.UsageError):
+        fodg.measure_graph(fodg.Graph(2, 1, np.array([[1], [7]], np.uint32)))
