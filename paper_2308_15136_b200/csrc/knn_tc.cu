@@ -66,6 +66,7 @@ constexpr int TC_EPI_WARPS = 4;
 #endif
 constexpr uint32_t TC_A_COL = 2 * 128;         // TS: A at TMEM columns [256, 256 + Kp/2)
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
+constexpr int TC_MAX_KB_STREAM = 64;  // beyond: query tile streamed with each data tile (SA)
 constexpr uint32_t TILE_BYTES = TC_BN * TC_BK * 2;  // 16 KB
 
 // ------------------------------------------------------------ PTX helpers --
@@ -249,13 +250,18 @@ struct TcArgs {
 // 128 query rows (A, smem) and loads HALF of the 128-point B tile; the leader
 // issues tcgen05.mma.cta_group::2 (M = 256) and each CTA's TMEM receives its
 // rows x all 128 points.  Per-SM B traffic from L2 halves.
-template <bool PAIR>
+// SA (K > 512, e.g. 960-d): the query tile does not fit next to the ring, so
+// every stage carries the A k-block together with the B k-block (a plain
+// streamed GEMM main loop; A is re-read from L2 once per data tile).
+template <bool PAIR, bool SA = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const TcArgs P) {
-  constexpr bool TS = CAGRA_KNN_TS && !PAIR;
+  static_assert(!(PAIR && SA), "streamed A is single-CTA");
+  constexpr bool TS = CAGRA_KNN_TS && !PAIR && !SA;
   constexpr int ACC = TS ? 2 : 4;
   constexpr uint32_t BTILE = PAIR ? TILE_BYTES / 2 : TILE_BYTES;  // B bytes per stage per CTA
+  constexpr uint32_t STAGE = SA ? 2 * TILE_BYTES : BTILE;         // [A k-block |] B k-block
   constexpr uint32_t idesc = PAIR ? ((1u << 4) | (1u << 7) | (1u << 10) |
                                      ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24))
                                   : kIdesc;
@@ -263,8 +269,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   // 1024-byte alignment for the SWIZZLE_128B tiles
   unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
   unsigned char* sA = base;                                   // SS: kblocks x 16 KB
-  unsigned char* sB = sA + (TS ? 0 : (size_t)P.kblocks * TILE_BYTES);  // stages x BTILE
-  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * BTILE);  // PEND x 128
+  unsigned char* sB = sA + (TS || SA ? 0 : (size_t)P.kblocks * TILE_BYTES);  // stages x STAGE
+  uint64_t* pend = reinterpret_cast<uint64_t*>(sB + P.stages * STAGE);  // PEND x 128
   uint64_t* bars = pend + P.pend_cap * TC_BM;
   // bars: full[S] empty[S] afull tfull[ACC] tempty[ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.stages + 1 + 2 * ACC);
@@ -333,6 +339,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           tma_load_2d_pair(smem_u32(sA + kb * TILE_BYTES), &tmA, afull, kb * TC_BK, row0);
         if (leader) mbar_expect_tx(afull, 2 * P.kblocks * TILE_BYTES);
         else mbar_arrive_remote(afull, 0);
+      } else if (SA) {
+        mbar_arrive(afull);  // nothing resident: A arrives with every stage
       } else if (!TS) {
         mbar_expect_tx(afull, P.kblocks * TILE_BYTES);
         for (uint32_t kb = 0; kb < P.kblocks; ++kb)
@@ -349,6 +357,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                              tile_of(t) * TC_BN + rank * (TC_BN / 2));
             if (leader) mbar_expect_tx(full0 + 8 * s, 2 * BTILE);
             else mbar_arrive_remote(full0 + 8 * s, 0);
+          } else if (SA) {
+            mbar_expect_tx(full0 + 8 * s, 2 * TILE_BYTES);
+            tma_load_2d(smem_u32(sB + s * STAGE), &tmA, full0 + 8 * s, kb * TC_BK, row0);
+            tma_load_2d(smem_u32(sB + s * STAGE + TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
+                        tile_of(t) * TC_BN);
           } else {
             mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
             tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
@@ -372,14 +385,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
-          const uint64_t bd = sw128_desc(smem_u32(sB + s * BTILE));
+          const uint64_t bd = sw128_desc(smem_u32(sB + s * STAGE + (SA ? TILE_BYTES : 0)));
           if (TS) {
 #pragma unroll
             for (uint32_t k = 0; k < TC_BK / 16; ++k)  // A: 16 bf16 = 8 TMEM columns per step
               tc_mma_ts(dcol, tmem + TC_A_COL + kb * (TC_BK / 2) + k * 8, bd + 2 * k, idesc,
                         (kb | k) != 0);
           } else {
-            const uint64_t ad = sw128_desc(smem_u32(sA + kb * TILE_BYTES));
+            const uint64_t ad = sw128_desc(smem_u32(SA ? sB + s * STAGE : sA + kb * TILE_BYTES));
 #pragma unroll
             for (uint32_t k = 0; k < TC_BK / 16; ++k) {  // 16 bf16 = 32 B = +2 in the address
               if (PAIR) tc_mma_pair(dcol, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
@@ -598,10 +611,43 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 // x = b0 + b1 + r,  |x|^2 = n0 + n1 + n2 (bf16 parts)
 //   query side P = [-2b0 | -2b0 | -2b1 | 1 1 1 | n0 n1 n2 | 0]
 //   data side  R = [  b0 |   b1 |   b0 | n0 n1 n2 | 1 1 1 | 0]
+// Column means of the dataset (the centring offset mu of the split), in two
+// fixed-order stages so mu is deterministic: per (32-column group, row chunk)
+// double partial sums, then a sequential sum over the chunks.
+constexpr uint32_t kMeanChunks = 256;
+__global__ void col_mean_partial_kernel(const float* __restrict__ data, uint32_t n, uint32_t ld,
+                                        uint32_t dim, double* __restrict__ part) {
+  const uint32_t col = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+  const uint32_t r0 = (uint32_t)((uint64_t)n * blockIdx.y / kMeanChunks);
+  const uint32_t r1 = (uint32_t)((uint64_t)n * (blockIdx.y + 1) / kMeanChunks);
+  double acc = 0.0;
+  if (col < dim)
+    for (uint32_t r = r0 + w; r < r1; r += blockDim.x / 32) acc += data[(size_t)r * ld + col];
+  __shared__ double red[8][32];
+  red[w][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (w == 0 && col < dim) {
+    double t = 0.0;
+    for (uint32_t k = 0; k < blockDim.x / 32; ++k) t += red[k][threadIdx.x];
+    part[(size_t)blockIdx.y * dim + col] = t;
+  }
+}
+__global__ void col_mean_final_kernel(const double* __restrict__ part, uint32_t n, uint32_t dim,
+                                      float* __restrict__ mu) {
+  const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= dim) return;
+  double t = 0.0;
+  for (uint32_t k = 0; k < kMeanChunks; ++k) t += part[(size_t)k * dim + col];
+  mu[col] = (float)(t / n);
+}
+
+// mu: the dataset mean, subtracted from every row (data and queries) before
+// the split.  Distances are translation-invariant; centring shrinks |x|, |q|
+// and with them the error bound delta, which matters at high dimension.
 __global__ void tc_split_kernel(const float* __restrict__ src, uint32_t rows, uint32_t ld,
-                                uint32_t dim, uint32_t Kp, __nv_bfloat16* __restrict__ P,
-                                __nv_bfloat16* __restrict__ R, float* __restrict__ norms,
-                                uint32_t* __restrict__ maxnorm_bits) {
+                                uint32_t dim, uint32_t Kp, const float* __restrict__ mu,
+                                __nv_bfloat16* __restrict__ P, __nv_bfloat16* __restrict__ R,
+                                float* __restrict__ norms, uint32_t* __restrict__ maxnorm_bits) {
   const uint32_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const uint32_t lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -611,7 +657,7 @@ __global__ void tc_split_kernel(const float* __restrict__ src, uint32_t rows, ui
   const __nv_bfloat16 zero = __float2bfloat16_rn(0.0f), one = __float2bfloat16_rn(1.0f);
   float ss = 0.0f;
   for (uint32_t i = lane; i < dim; i += 32) {
-    float v = x[i];
+    float v = x[i] - mu[i];
     ss = fmaf(v, v, ss);
     __nv_bfloat16 b0 = __float2bfloat16_rn(v);
     __nv_bfloat16 b1 = __float2bfloat16_rn(v - __bfloat162float(b0));
@@ -892,11 +938,15 @@ CUtensorMap make_map(const void* base, uint32_t rows, uint32_t Kp, uint32_t row_
   return tm;
 }
 
+// the query tile is streamed (SA) when it cannot stay resident
+bool tc_streamed(uint32_t kblocks) { return kblocks > TC_MAX_KB; }
+
 size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_PEND,
                      bool pair = false) {
-  const bool ts = CAGRA_KNN_TS && !pair;
-  const size_t btile = pair ? TILE_BYTES / 2 : TILE_BYTES;
-  return 1024 + (ts ? 0 : (size_t)kblocks * TILE_BYTES) + stages * btile +
+  const bool sa = tc_streamed(kblocks);
+  const bool ts = CAGRA_KNN_TS && !pair && !sa;
+  const size_t stage = sa ? 2 * TILE_BYTES : (pair ? TILE_BYTES / 2 : TILE_BYTES);
+  return 1024 + (ts || sa ? 0 : (size_t)kblocks * TILE_BYTES) + stages * stage +
          sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * (ts ? 2 : 4)) + 16;
 }
 
@@ -917,9 +967,10 @@ bool knn_tc_eligible(uint32_t dim, uint32_t K) {
   const char* env = std::getenv("CAGRA_KNN_PATH");
   if (env && std::strcmp(env, "simt") == 0) return false;
   uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK);
-  return Kp / TC_BK <= TC_MAX_KB &&
-         tc_smem_bytes(Kp / TC_BK, tc_stages(Kp / TC_BK, TC_PEND, true), TC_PEND, true) <= kSmemLimit &&
-         K + 32 + TC_PEND <= 256;
+  const uint32_t kb = Kp / TC_BK;
+  if (kb > TC_MAX_KB_STREAM || K + 32 + TC_PEND > 256) return false;
+  if (tc_streamed(kb)) return tc_smem_bytes(kb, 3) <= kSmemLimit;  // >= 3-deep A+B ring
+  return tc_smem_bytes(kb, tc_stages(kb, TC_PEND, true), TC_PEND, true) <= kSmemLimit;
 }
 
 namespace {
@@ -943,7 +994,8 @@ bool tc_pair_enabled() {
 
 void run_tc_kernel(const TcCall& c, const void* Pq, const CUtensorMap& tmA,
                    const CUtensorMap& tmB, TcArgs a, uint32_t nq) {
-  const bool pair = tc_pair_enabled();
+  const bool sa = tc_streamed(c.kblocks);
+  const bool pair = tc_pair_enabled() && !sa;
   a.kblocks = c.kblocks;
   a.prow = reinterpret_cast<const uint32_t*>(Pq);
   const char* ge = std::getenv("CAGRA_TC_GROUPS");
@@ -953,6 +1005,14 @@ void run_tc_kernel(const TcCall& c, const void* Pq, const CUtensorMap& tmA,
   a.exclude_self = c.exclude_self ? 1 : 0;
   a.nq = nq;
   const size_t smem = tc_smem_bytes(c.kblocks, a.stages, a.pend_cap, pair);
+  if (sa) {
+    CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    knn_tc_kernel<false, true>
+        <<<(nq + TC_BM - 1) / TC_BM, TC_THREADS, smem, c.stream>>>(tmA, tmB, a);
+    CAGRA_LAUNCH_CHECK();
+    return;
+  }
   if (!pair) {
     CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -988,7 +1048,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   Dev lists(8ull * nq * KC), fails(4ull * nq + 4), rer(8);
   CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, c.stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, c.stream));
-  const uint32_t brows = tc_pair_enabled() ? TC_BN / 2 : TC_BN;
+  const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
   CUtensorMap tmA = make_map(P, nq, c.Kp, 1), tmB = make_map(c.R, c.n, c.Kp, 1, brows);
   TcArgs a{};
   a.n = c.n;
@@ -1057,18 +1117,26 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   c.exclude_self = exclude_self;
   c.stream = stream;
   // error bound of d~ (file header): |d~ - d| <= eps_rel |q| max|x| +
-  // eps_norm (|q|^2 + max|x|^2): the split's omitted terms (3.1*2^-16 of
-  // sum|q_i||x_i| <= |q||x|, doubled by the -2), fp32 accumulation over Kp
-  // terms of total magnitude 2|q||x| + |q|^2 + |x|^2, and the fp32 norms.
+  // eps_norm (|q|^2 + max|x|^2), norms of the centred rows x' = fl(x - mu):
+  // the split's omitted terms (3.1*2^-16 of sum|q_i||x_i| <= |q||x|, doubled
+  // by the -2), fp32 accumulation over Kp terms of total magnitude
+  // 2|q||x| + |q|^2 + |x|^2, the fp32 norms, and the centring rounding
+  // (|d - |x'-q'|^2| <= 2u (|x'| + |q'|)^2, u = 2^-24; counted with 2^-23).
   const float u23 = 1.1920929e-07f;
-  c.eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)c.Kp * u23;
-  c.eps_norm = (float)c.Kp * u23 + (float)(dim + 8) * u23;
+  c.eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)c.Kp * u23 + 4.0f * u23;
+  c.eps_norm = (float)c.Kp * u23 + (float)(dim + 8) * u23 + 2.0f * u23;
 
   const bool same = exclude_self;  // kNN graph: queries are the data rows
   Dev dP((size_t)nq * c.Kp * 2), dR((size_t)n * c.Kp * 2), dqn(4ull * nq), dxn(4ull * n), dmax(4);
   CAGRA_CUDA_TRY(cudaMemsetAsync(dmax.p, 0, 4, stream));
+  Dev dmu(4ull * dim), dpart(8ull * kMeanChunks * dim);
+  col_mean_partial_kernel<<<dim3((dim + 31) / 32, kMeanChunks), 256, 0, stream>>>(
+      d_data, n, ld, dim, dpart.as<double>());
+  col_mean_final_kernel<<<(dim + 127) / 128, 128, 0, stream>>>(dpart.as<double>(), n, dim,
+                                                               dmu.as<float>());
+  CAGRA_LAUNCH_CHECK();
   // data side: R (and P when the queries are the data), norms, max norm
-  tc_split_kernel<<<(n + 7) / 8, 256, 0, stream>>>(d_data, n, ld, dim, c.Kp,
+  tc_split_kernel<<<(n + 7) / 8, 256, 0, stream>>>(d_data, n, ld, dim, c.Kp, dmu.as<float>(),
                                                    same ? dP.as<__nv_bfloat16>() : nullptr,
                                                    dR.as<__nv_bfloat16>(), dxn.as<float>(),
                                                    dmax.as<uint32_t>());
@@ -1076,7 +1144,8 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   const float* qnorm = dxn.as<float>();
   if (!same) {
     tc_split_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(d_queries, nq, qld, dim, c.Kp,
-                                                      dP.as<__nv_bfloat16>(), nullptr,
+                                                      dmu.as<float>(), dP.as<__nv_bfloat16>(),
+                                                      nullptr,
                                                       dqn.as<float>(), nullptr);
     CAGRA_LAUNCH_CHECK();
     qnorm = dqn.as<float>();
@@ -1100,7 +1169,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, stream));
     CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
     CAGRA_CUDA_TRY(cudaMemsetAsync(bcount.p, 0, 4ull * nq, stream));  // append counters
-    const uint32_t brows = tc_pair_enabled() ? TC_BN / 2 : TC_BN;
+    const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
     CUtensorMap tmA = make_map(dP.p, nq, c.Kp, 1);
     CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride, brows);
     CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1, brows);

@@ -79,6 +79,8 @@ def test_knn_odd_dimension_and_ragged_tiles(gpu, oracle):
     (3000, 128, 64, False),    # single pass, D=128 (7 K-blocks, 3-stage ring)
     (70000, 96, 128, True),    # sample pass + append pass (DEEP shape, d_init 128)
     (90000, 37, 40, True),     # odd dim, ragged last tile
+    (4000, 200, 32, False),    # K = 640 > 512: query tile streamed with each data tile
+    (70000, 960, 128, True),   # GIST shape, streamed query tile, both passes
 ])
 def test_knn_tensor_core_path_bit_exact(gpu, oracle, monkeypatch, n, dim, k, two_pass):
     # K1 on tcgen05 (knn_tc.cu) against the SIMT sequential-chain kernel (itself
@@ -430,8 +432,8 @@ def test_search_random_params_vs_oracle(gpu, oracle):
 # ------------------------------------------------- GIST-shaped (C3) parity ----
 def test_gist_shape_960d_pipeline_vs_oracle(gpu, oracle):
     """BASELINE configs[2] shape (960-d, graph degree 64, multi-CTA small
-    batch) at oracle-checkable size: the kNN graph (SIMT sequential-chain path:
-    K = 3*960+6 exceeds the tensor-core tile) and the optimized graph are
+    batch) at oracle-checkable size: the kNN graph (tensor-core path with the
+    query tile streamed: K = 3*960+6 > 512) and the optimized graph are
     bit-exact; per-query search in reference-semantics mode matches the oracle
     exactly; multi-CTA shared mode is within 0.5 pp of the reference's shared
     mode."""
