@@ -48,20 +48,23 @@ def main():
     grid = []
     if args.grid:
         for tok in args.grid.split(";"):
-            m, p, pol, bits, ts, ri = (tok.split(",") + ["0", "0", "0", "1"])[:6]
-            grid.append((int(m), int(p), int(pol), int(bits), int(ts), int(ri)))
+            # M,p,policy,bits,team_size,reset_interval[,mode,teams,multi_cta]
+            defaults = [0, 0, 0, 0, 0, 1, 0, 4, 0]
+            vals = [int(x) for x in tok.split(",")]
+            grid.append(tuple(vals + defaults[len(vals):]))
     else:
         for m, p in [(512, 8), (768, 16), (896, 16), (1024, 16), (1024, 32)]:
             for pol in (0, 1):
                 for ts in (4, 8, 16):
-                    grid.append((m, p, pol, 0, ts, 1))
-    for (m, p, pol, bits, ts, ri) in grid:
+                    grid.append((m, p, pol, 0, ts, 1, 0, 4, 0))
+    for (m, p, pol, bits, ts, ri, mode, teams, mc) in grid:
         if not bits:
             need = m + p * args.d
             bits = max(10, int(np.ceil(np.log2(need * 1.6))))
         prm = fodg.SearchParams(k=10, topm=m, width=p, hash_policy=fodg.HashPolicy(pol),
                                 hash_bits=bits, seed=11, reset_interval=ri)
-        opt = fodg.EngineOptions(team_size=ts)
+        opt = fodg.EngineOptions(team_size=ts, mode=fodg.ExecutionMode(mode), team_count=teams,
+                                 multi_cta=mc)
         try:
             ix.search_dev(qd, args.nq, prm, opt, ids, dists, None, stats, stream)
             torch.cuda.synchronize()
@@ -84,7 +87,8 @@ def main():
         rec = np.mean([len(set(hid[i]) & set(gt[i])) / 10 for i in range(args.nq)])
         bytes_q = evals.mean() * args.dim * 4 + iters.mean() * p * args.d * 4
         gbs = bytes_q * args.nq / (ms * 1e-3) / 1e9
-        print(f"M={m:5d} p={p:3d} pol={pol} bits={bits:2d} ts={ts} ri={ri} recall={rec:.4f} "
+        print(f"M={m:5d} p={p:3d} pol={pol} bits={bits:2d} ts={ts} ri={ri} mode={mode} "
+              f"teams={teams} mc={mc} recall={rec:.4f} "
               f"qps={args.nq / (ms * 1e-3):10.0f} ms={ms:8.2f} evals={evals.mean():8.0f} "
               f"iters={iters.mean():6.1f} alg_GBs={gbs:7.0f}", flush=True)
 
