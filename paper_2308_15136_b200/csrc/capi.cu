@@ -272,6 +272,12 @@ SearchConfig to_config(const cagra_search_params* p, const cagra_engine_opts* o)
 
 constexpr size_t kTableBudget = 8ull << 30;
 
+// kTableBudget, or CAGRA_TABLE_BUDGET_MB (tests exercise the chunked paths)
+size_t table_budget() {
+  const char* e = std::getenv("CAGRA_TABLE_BUDGET_MB");
+  return e && *e ? (size_t)std::strtoull(e, nullptr, 10) << 20 : kTableBudget;
+}
+
 // Runs a search on device-resident queries (rows of ix->ld floats).
 void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
                 const cagra_search_params* params, const cagra_engine_opts* opts,
@@ -280,12 +286,30 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
   DeviceIndexView v{ix->data.as<float>(), ix->graph.as<uint32_t>(), ix->n, ix->dim, ix->ld,
                     ix->degree};
   SearchConfig c = to_config(params, opts);
+  if (c.mode == 1 && !c.exact && c.multi_cta == 2 && nq > 1) {
+    // forced multi-CTA on a large batch: chunks whose per-query visited
+    // regions fit the table budget (query_offset keeps the seeds global)
+    const uint64_t maxq =
+        std::max<uint64_t>(1, table_budget() / mc_table_bytes_per_query(c, ix->degree));
+    if (nq > maxq) {
+      const size_t k = params->k;
+      cagra_engine_opts o = *opts;
+      for (uint64_t off = 0; off < nq; off += maxq) {
+        const uint32_t m = (uint32_t)std::min<uint64_t>(maxq, nq - off);
+        o.query_offset = opts->query_offset + off;
+        run_search(ix, d_queries + off * ix->ld, m, params, &o, d_ids + off * k,
+                   d_dists + off * k, d_counts ? d_counts + off : nullptr,
+                   d_stats ? static_cast<cagra_search_stats*>(d_stats) + off : nullptr, s);
+      }
+      return;
+    }
+  }
   // the plan (kernel variant, grid, smem, table sizes) depends only on the
   // configuration and the batch size: reuse it across repeated calls
   // (batch-1 loops) instead of re-querying attributes and occupancy
   if (!ix->plan_valid || ix->plan_nq != nq ||
       std::memcmp(&ix->plan_cfg, &c, sizeof(SearchConfig)) != 0) {
-    ix->plan = plan_search(v, c, nq, ix->sm_count, kTableBudget);
+    ix->plan = plan_search(v, c, nq, ix->sm_count, table_budget());
     ix->plan_cfg = c;
     ix->plan_nq = nq;
     ix->plan_valid = true;

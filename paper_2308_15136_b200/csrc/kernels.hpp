@@ -107,6 +107,8 @@ struct SearchPlan {
   const void* fn = nullptr;
 };
 // Validates device limits and picks the kernel variant / grid.
+// bytes of one query's multi-CTA visited region (shared by its teams)
+uint64_t mc_table_bytes_per_query(const SearchConfig& c, uint32_t degree);
 SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_t nq,
                        int sm_count, size_t table_budget_bytes);
 // Launches init-sample + search kernels; returns the number of kernels.

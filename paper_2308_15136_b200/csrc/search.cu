@@ -1460,6 +1460,15 @@ KernelFn shared_fn(bool exact, Variant v) {
 
 }  // namespace
 
+uint64_t mc_table_bytes_per_query(const SearchConfig& c, uint32_t degree) {
+  // the shared-mode visited table of plan_search (engine.cpp:47-50)
+  const uint32_t imax = resolved_max_iter(c.max_iter, c.topm, 1);
+  const uint64_t want = 2 * std::max<uint64_t>(1, (uint64_t)(imax + 1) * c.team_count * degree);
+  uint64_t cap = 1;
+  while (cap < want) cap <<= 1;
+  return cap * 8;
+}
+
 SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_t nq,
                        int sm_count, size_t table_budget) {
   SearchPlan pl;

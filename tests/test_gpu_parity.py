@@ -538,3 +538,28 @@ def test_graph_metrics_vs_reference(gpu, oracle, reference):
         assert rep.max_2hop == d * (1 + d)
     with pytest.raises(fodg.UsageError):
         fodg.measure_graph(fodg.Graph(2, 1, np.array([[1], [7]], np.uint32)))
+
+
+def test_multi_cta_large_batch_chunked(gpu, oracle, monkeypatch):
+    # forced multi-CTA on a batch whose per-query visited regions exceed the
+    # table budget runs in query chunks (query_offset keeps seeds global):
+    # same recall as one launch
+    data = oracle.uniform_dataset(20000, 32, 7)
+    queries = oracle.uniform_dataset(300, 32, 8)
+    ds = fodg.Dataset.from_array(data)
+    g, _ = fodg.build_graph(ds, 32)
+    gt, _ = fodg.exact_topk_batch(ds, queries, 10)
+    ix = fodg.Index(ds, g)
+    prm = fodg.SearchParams(k=10, topm=64, width=1, seed=3)
+    opts = fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers, team_count=8,
+                              multi_cta=2)
+
+    def recall(ids):
+        return np.mean([len(set(ids[q]) & set(gt[q])) / 10 for q in range(len(gt))])
+
+    one = ix.search(queries, prm, opts)
+    monkeypatch.setenv("CAGRA_TABLE_BUDGET_MB", "4")  # 1 MB per query -> chunks of 4
+    chunked = ix.search(queries, prm, opts)
+    assert np.all(chunked[2] == 10)
+    assert np.all(chunked[3]["iterations"] > 0)
+    assert abs(recall(one[0]) - recall(chunked[0])) <= 0.01
