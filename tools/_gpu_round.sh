@@ -5,7 +5,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/sm
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
 timeout 900 python bench.py > gpurun_out/bench_ours.json 2> gpurun_out/bench_ours.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01c.csv python bench.py --steps 2 --warmup 3 --no-cpu --batch1 20 > gpurun_out/ncu_launch_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:search_kernel -s 3 -c 1 -o gpurun_out/search_full3 python bench.py --steps 1 --warmup 3 --no-cpu --batch1 0 > gpurun_out/ncu_full.log 2>&1
+timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01d.csv python bench.py --steps 2 --warmup 3 --no-cpu --batch1 20 > gpurun_out/ncu_launch_bench.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:search_kernel -s 3 -c 1 -o gpurun_out/search_full4 python bench.py --steps 1 --warmup 3 --no-cpu --batch1 0 > gpurun_out/ncu_full.log 2>&1
 ${EXTRA_CMD:-true}
 ls -la gpurun_out
