@@ -259,12 +259,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
               const TcArgs P) {
   static_assert(!(PAIR && SA), "streamed A is single-CTA");
   constexpr bool TS = CAGRA_KNN_TS && !PAIR && !SA;
-  constexpr int ACC = TS ? 2 : 4;
+  // SA data tiles are 256 points wide (one N=256 MMA per k-block), so every
+  // streamed A k-block is used against two 128-point B tiles
+  constexpr uint32_t W = SA ? 2 * TC_BN : TC_BN;  // data points per tile
+  constexpr int ACC = TS || SA ? 2 : 4;           // W-column accumulators in 512 TMEM columns
   constexpr uint32_t BTILE = PAIR ? TILE_BYTES / 2 : TILE_BYTES;  // B bytes per stage per CTA
-  constexpr uint32_t STAGE = SA ? 2 * TILE_BYTES : BTILE;         // [A k-block |] B k-block
+  constexpr uint32_t STAGE = SA ? 3 * TILE_BYTES : BTILE;         // [A k-block |] B k-block(s)
   constexpr uint32_t idesc = PAIR ? ((1u << 4) | (1u << 7) | (1u << 10) |
                                      ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24))
-                                  : kIdesc;
+                           : SA ? ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(W >> 3) << 17) |
+                                   ((uint32_t)(TC_BM >> 4) << 24))
+                                : kIdesc;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B tiles
   unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
@@ -279,7 +284,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const uint32_t row0 = PAIR ? (blockIdx.x >> 1) * 2 * TC_BM + rank * TC_BM : blockIdx.x * TC_BM;
-  const uint32_t ntiles = (P.n + TC_BN - 1) / TC_BN;
+  const uint32_t ntiles = (P.n + W - 1) / W;
   const uint32_t S = P.stages;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
   const uint32_t afull = smem_u32(bars + 2 * S);
@@ -358,10 +363,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (leader) mbar_expect_tx(full0 + 8 * s, 2 * BTILE);
             else mbar_arrive_remote(full0 + 8 * s, 0);
           } else if (SA) {
-            mbar_expect_tx(full0 + 8 * s, 2 * TILE_BYTES);
+            // A k-block, then the two 128-row halves of the 256-point B k-block
+            // back to back (one K-major SWIZZLE_128B operand of 256 rows)
+            mbar_expect_tx(full0 + 8 * s, 3 * TILE_BYTES);
             tma_load_2d(smem_u32(sB + s * STAGE), &tmA, full0 + 8 * s, kb * TC_BK, row0);
             tma_load_2d(smem_u32(sB + s * STAGE + TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
-                        tile_of(t) * TC_BN);
+                        tile_of(t) * W);
+            tma_load_2d(smem_u32(sB + s * STAGE + 2 * TILE_BYTES), &tmB, full0 + 8 * s,
+                        kb * TC_BK, tile_of(t) * W + TC_BN);
           } else {
             mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
             tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
@@ -380,7 +389,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t acc = t % ACC, aph = (t / ACC) & 1;
         mbar_wait(tempty0 + 8 * acc, aph ^ 1);
         tc_fence_after();
-        const uint32_t dcol = tmem + acc * TC_BN;
+        const uint32_t dcol = tmem + acc * W;
         for (uint32_t kb = 0; kb < P.kblocks; ++kb, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(full0 + 8 * s, ph);
@@ -413,7 +422,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t row = row0 + rl;
     const bool live = row < P.nq;
     uint64_t* mypend = pend;
-    const uint32_t c_lo = 0, c_hi = TC_BN / 32;
+    const uint32_t c_lo = 0, c_hi = W / 32;
     if (TS) {
       // this row of A -> TMEM lane rl, columns [TC_A_COL, TC_A_COL + Kp/2)
       const uint32_t half = P.kblocks * (TC_BK / 2);
@@ -521,7 +530,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll 1
       for (uint32_t c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
-        tmem_ld32_nowait(tmem + ((q4 * 32) << 16) + acc * TC_BN + c * 32, v);
+        tmem_ld32_nowait(tmem + ((q4 * 32) << 16) + acc * W + c * 32, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == c_hi - 1) {
           // release the accumulator: one arrival per warp, at the leader for a pair
@@ -559,7 +568,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (!__any_sync(0xffffffffu, hit)) continue;
         // slow path: only the FMNMX3 groups whose minimum passes are
         // examined element by element (appends are rare after the first tiles)
-        const uint32_t cbase = tile_of(t) * TC_BN + c * 32;
+        const uint32_t cbase = tile_of(t) * W + c * 32;
         if (hit) {
           auto take = [&](int i) {
             const float d = __uint_as_float(v[i]);
@@ -945,9 +954,9 @@ size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_P
                      bool pair = false) {
   const bool sa = tc_streamed(kblocks);
   const bool ts = CAGRA_KNN_TS && !pair && !sa;
-  const size_t stage = sa ? 2 * TILE_BYTES : (pair ? TILE_BYTES / 2 : TILE_BYTES);
+  const size_t stage = sa ? 3 * TILE_BYTES : (pair ? TILE_BYTES / 2 : TILE_BYTES);
   return 1024 + (ts || sa ? 0 : (size_t)kblocks * TILE_BYTES) + stages * stage +
-         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * (ts ? 2 : 4)) + 16;
+         sizeof(uint64_t) * (pend_cap * TC_BM + 2 * stages + 1 + 2 * (ts || sa ? 2 : 4)) + 16;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -969,7 +978,7 @@ bool knn_tc_eligible(uint32_t dim, uint32_t K) {
   uint32_t Kp = round_up_u32(3 * dim + 6, TC_BK);
   const uint32_t kb = Kp / TC_BK;
   if (kb > TC_MAX_KB_STREAM || K + 32 + TC_PEND > 256) return false;
-  if (tc_streamed(kb)) return tc_smem_bytes(kb, 3) <= kSmemLimit;  // >= 3-deep A+B ring
+  if (tc_streamed(kb)) return tc_smem_bytes(kb, 3) <= kSmemLimit;  // >= 3-deep A+B+B ring
   return tc_smem_bytes(kb, tc_stages(kb, TC_PEND, true), TC_PEND, true) <= kSmemLimit;
 }
 
