@@ -1,5 +1,6 @@
-"""compute-sanitizer over a small run of every kernel family (tensor-core and
-SIMT kNN, rank optimize, per-query / lockstep / multi-CTA search in both
+"""compute-sanitizer over a small run of every kernel family (tensor-core kNN
+with resident and streamed query tiles, SIMT kNN, rank optimize, graph
+metrics, per-query / lockstep / multi-CTA search in both
 distance modes and both visited policies): no memory errors, no shared-memory
 races, no illegal barrier use, no uninitialised device reads."""
 import os

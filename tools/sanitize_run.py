@@ -26,4 +26,7 @@ for mc in (1, 2):
     ix.search(q, fodg.SearchParams(k=5, topm=16, width=1, seed=3),
               fodg.EngineOptions(mode=fodg.ExecutionMode.kSharedQueryWorkers, team_count=4,
                                  multi_cta=mc))
+ds2 = fodg.Dataset.from_array(capi.uniform_dataset(700, 200, 4))   # K > 512: streamed query tile
+fodg.exact_knn_graph(ds2, 16)
+fodg.measure_graph(g)                                                   # graph metrics (SCC + 2-hop)
 print("sanitize run ok")
