@@ -77,3 +77,16 @@ def test_argument_validation_precedes_device_use():
     g = fodg.KnnGraph(2, 1, np.array([[1], [0]], np.uint32), np.ones((2, 1), np.float32))
     with pytest.raises(capi.UsageError):
         fodg.optimize(g, 2)
+
+
+def test_graph_metrics_host_side():
+    # graph_metrics.hpp: empty graph needs no device; the report is the
+    # reference's key=value lines; compute needs the device (no CPU fallback)
+    empty = fodg.Graph(0, 4, np.zeros((0, 4), np.uint32))
+    r = fodg.measure_graph(empty)
+    assert (r.strong_cc, r.avg_2hop, r.max_2hop) == (0, 0.0, 20)
+    assert fodg.GraphQualityReport(3, 2, 1, 1.5, 6).report() == (
+        "num_nodes=3\ndegree=2\nstrong_cc=1\navg_2hop=1.5\nmax_2hop=6\n")
+    if capi.device_count() == 0:
+        with pytest.raises(capi.CudaError):
+            fodg.measure_graph(fodg.Graph(2, 1, np.array([[1], [0]], np.uint32)))
