@@ -84,9 +84,6 @@ struct DBuf {
     CAGRA_CUDA_TRY(cudaMalloc(&p, b));
     bytes = b;
   }
-  void ensure(size_t b) {
-    if (b > bytes) alloc(b);
-  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -226,10 +223,33 @@ struct cagra_index {
   uint32_t plan_nq = 0;
   bool plan_valid = false;
   bool mc_layout = false;     // tables currently laid out per query
-  ~cagra_index() { delete stream; }
+  // Completion of the last search issued on this index, on whatever stream
+  // it ran.  Every search first makes its stream wait on it and records it
+  // again at the end, so calls on different streams (cagra_search on the
+  // private stream, cagra_search_dev on caller streams) never overlap on the
+  // per-index scratch, and a scratch buffer is only reallocated once the
+  // work that used it has finished (grow()).
+  cudaEvent_t done = nullptr;
+  ~cagra_index() {
+    if (done) cudaEventDestroy(done);
+    delete stream;
+  }
 };
 
 namespace {
+
+// Grows a per-index scratch buffer after the index's previous search is done.
+void grow(cagra_index* ix, DBuf& b, size_t bytes) {
+  if (bytes <= b.bytes) return;
+  CAGRA_CUDA_TRY(cudaEventSynchronize(ix->done));
+  b.alloc(bytes);
+}
+
+// Orders this call's work on `s` after every earlier search on the index.
+void begin_on(cagra_index* ix, cudaStream_t s) {
+  CAGRA_CUDA_TRY(cudaStreamWaitEvent(s, ix->done, 0));
+}
+void end_on(cagra_index* ix, cudaStream_t s) { CAGRA_CUDA_TRY(cudaEventRecord(ix->done, s)); }
 
 void validate_params(const cagra_search_params* p) {
   // SearchParams::validate (search.cpp:39-50), same order
@@ -315,38 +335,38 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
     ix->plan_valid = true;
   }
   const SearchPlan& pl = ix->plan;
-  ix->init_ids.ensure(sizeof(uint32_t) * std::max<size_t>(pl.init_elems, 1));
-  ix->work.ensure(sizeof(uint32_t));
+  grow(ix, ix->init_ids, sizeof(uint32_t) * std::max<size_t>(pl.init_elems, 1));
+  grow(ix, ix->work, sizeof(uint32_t));
   if (pl.mc) {
-    ix->team_out.ensure(sizeof(unsigned long long) * std::max<size_t>(pl.team_elems, 1));
-    ix->team_stats.ensure(sizeof(cagra_search_stats) * (size_t)nq * pl.teams);
+    grow(ix, ix->team_out, sizeof(unsigned long long) * std::max<size_t>(pl.team_elems, 1));
+    grow(ix, ix->team_stats, sizeof(cagra_search_stats) * (size_t)nq * pl.teams);
     // per-query regions tagged by a call generation; a new layout starts clean
     if (!ix->mc_layout || pl.hcap != ix->table_hcap || pl.table_elems > ix->table_elems ||
         ix->mc_tag == 0xffffffffu) {
       if (pl.table_elems > ix->table_elems) {
-        ix->tables.alloc(sizeof(unsigned long long) * pl.table_elems);
+        grow(ix, ix->tables, sizeof(unsigned long long) * pl.table_elems);
         ix->table_elems = pl.table_elems;
       }
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->tables.p, 0, ix->tables.bytes, s));
       ix->mc_tag = 0;
       ix->table_hcap = pl.hcap;
       ix->table_grid = 0;  // the per-CTA generations no longer match
-      ix->gens.ensure(sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
+      grow(ix, ix->gens, sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
       ix->mc_layout = true;
     }
     ix->mc_tag++;
-    ix->gens.ensure(sizeof(uint32_t) * pl.grid);
+    grow(ix, ix->gens, sizeof(uint32_t) * pl.grid);
   } else if (pl.table_elems) {
     bool relayout = ix->mc_layout || pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
                     pl.table_elems > ix->table_elems;
     if (relayout) {
       // a changed layout would alias old tags into other slots: start clean
       if (pl.table_elems > ix->table_elems) {
-        ix->tables.alloc(sizeof(unsigned long long) * pl.table_elems);
+        grow(ix, ix->tables, sizeof(unsigned long long) * pl.table_elems);
         ix->table_elems = pl.table_elems;
       }
-      ix->gens.ensure(sizeof(uint32_t) * std::max<uint32_t>(pl.grid, ix->table_grid));
+      grow(ix, ix->gens, sizeof(uint32_t) * std::max<uint32_t>(pl.grid, ix->table_grid));
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->tables.p, 0, ix->tables.bytes, s));
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
       ix->table_hcap = pl.hcap;
@@ -354,7 +374,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
       ix->mc_layout = false;
     }
   } else {
-    ix->gens.ensure(sizeof(uint32_t) * pl.grid);
+    grow(ix, ix->gens, sizeof(uint32_t) * pl.grid);
   }
   ix->last_launches = launch_search(v, c, pl, d_queries, nq, d_ids, d_dists, d_counts, d_stats,
                                     ix->init_ids.as<uint32_t>(), ix->work.as<uint32_t>(),
@@ -712,6 +732,7 @@ static void create_index(const float* data, uint32_t n, uint32_t dim, const uint
     ix->ld = row_stride(dim);
     ix->degree = degree;
     ix->stream = new Stream();
+    CAGRA_CUDA_TRY(cudaEventCreateWithFlags(&ix->done, cudaEventDisableTiming));
     cudaStream_t s = ix->stream->s;
     ix->data.alloc(sizeof(float) * (size_t)n * ix->ld);
     ix->graph.alloc(sizeof(uint32_t) * (size_t)n * degree);
@@ -725,6 +746,7 @@ static void create_index(const float* data, uint32_t n, uint32_t dim, const uint
     int h = 0;
     read_flag(flag.as<int>(), &h, s);
     if (h) throw UsageErr("search: graph/dataset size mismatch (neighbour id out of range)");
+    end_on(ix, s);
   } catch (...) {
     delete ix;
     throw;
@@ -783,11 +805,12 @@ int cagra_search(cagra_index* ix, const float* queries, uint32_t nq, uint32_t di
     DeviceScope scope(ix->device);
     cudaStream_t s = ix->stream->s;
     const uint32_t k = params->k;
-    ix->q.ensure(sizeof(float) * (size_t)nq * ix->ld);
-    ix->ids.ensure(sizeof(uint32_t) * (size_t)nq * k);
-    ix->dists.ensure(sizeof(float) * (size_t)nq * k);
-    ix->counts.ensure(sizeof(uint32_t) * nq);
-    ix->stats.ensure(sizeof(cagra_search_stats) * nq);
+    begin_on(ix, s);
+    grow(ix, ix->q, sizeof(float) * (size_t)nq * ix->ld);
+    grow(ix, ix->ids, sizeof(uint32_t) * (size_t)nq * k);
+    grow(ix, ix->dists, sizeof(float) * (size_t)nq * k);
+    grow(ix, ix->counts, sizeof(uint32_t) * nq);
+    grow(ix, ix->stats, sizeof(cagra_search_stats) * nq);
     upload_rows(ix->q.as<float>(), queries, nq, dim, ix->ld, s);
     run_search(ix, ix->q.as<float>(), nq, params, o, ix->ids.as<uint32_t>(),
                ix->dists.as<float>(), ix->counts.as<uint32_t>(), ix->stats.p, s);
@@ -801,6 +824,7 @@ int cagra_search(cagra_index* ix, const float* queries, uint32_t nq, uint32_t di
     if (stats_out)
       CAGRA_CUDA_TRY(cudaMemcpyAsync(stats_out, ix->stats.p, sizeof(cagra_search_stats) * nq,
                                      cudaMemcpyDeviceToHost, s));
+    end_on(ix, s);
     CAGRA_CUDA_TRY(cudaStreamSynchronize(s));
   });
 }
@@ -820,13 +844,16 @@ int cagra_search_dev(cagra_index* ix, const float* d_queries, uint32_t nq,
       throw UsageErr("batch_search: shared mode requires team_count >= 2");
     std::lock_guard<std::mutex> lock(ix->mu);
     DeviceScope scope(ix->device);
-    cudaStream_t s = stream ? reinterpret_cast<cudaStream_t>(stream) : ix->stream->s;
+    // NULL = the caller's legacy default stream (CUDA's usual convention)
+    cudaStream_t s = stream ? reinterpret_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    begin_on(ix, s);
     uint32_t* counts = d_counts_out;
     if (!counts) {
-      ix->counts.ensure(sizeof(uint32_t) * nq);
+      grow(ix, ix->counts, sizeof(uint32_t) * nq);
       counts = ix->counts.as<uint32_t>();
     }
     run_search(ix, d_queries, nq, params, o, d_ids_out, d_dists_out, counts, d_stats_out, s);
+    end_on(ix, s);
   });
 }
 

@@ -12,11 +12,13 @@ namespace cagra {
 // ---- knn_exact.cu / knn_tc.cu -----------------------------------------------
 // Exact top-K by (dist, id) for nq query rows against n data rows (row
 // strides ld / qld floats).  exclude_self drops data index == the query's own
-// index (the kNN graph, knn_build.cpp:52-60): self_ids[qi] when given, else qi.
+// index (the kNN graph, knn_build.cpp:52-60): query row qi is data row
+// self_base + qi (row-sharded builds pass d_queries = d_data + self_base * ld).
 // Dispatcher: the tensor-core path (knn_tc.cu) when eligible, else SIMT.
 void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                        uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                       uint32_t* d_ids, float* d_dists, cudaStream_t stream);
+                       uint32_t* d_ids, float* d_dists, cudaStream_t stream,
+                       uint32_t self_base = 0);
 // SIMT register-tiled sequential-chain kernel.  d_topk_scratch: nq*K u64.
 void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                             uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K,
@@ -27,7 +29,7 @@ void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const 
 bool knn_tc_eligible(uint32_t dim, uint32_t K);
 void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                   uint32_t* d_ids, float* d_dists, cudaStream_t stream);
+                   uint32_t self_base, uint32_t* d_ids, float* d_dists, cudaStream_t stream);
 struct KnnTcStats {
   uint64_t rows = 0, fallback_rows = 0, reranked = 0, retried_rows = 0;
 };

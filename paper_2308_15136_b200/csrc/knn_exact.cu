@@ -213,6 +213,11 @@ size_t exact_topk_smem(uint32_t K) {
 
 }  // namespace
 
+__global__ void iota_kernel(uint32_t* __restrict__ out, uint32_t cnt, uint32_t base) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) out[i] = base + i;
+}
+
 void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                             uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K,
                             bool exclude_self, const uint32_t* d_self_ids,
@@ -232,21 +237,28 @@ void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const 
 
 void launch_exact_topk(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                        uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                       uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
+                       uint32_t* d_ids, float* d_dists, cudaStream_t stream, uint32_t self_base) {
   if (K > MAX_K) throw UsageErr("device exact top-k supports k <= 1024");
   if (nq == 0) return;
   if (knn_tc_eligible(dim, K)) {
-    launch_knn_tc(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, d_ids, d_dists,
-                  stream);
+    launch_knn_tc(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, self_base, d_ids,
+                  d_dists, stream);
     return;
   }
   g_knn_tc_stats = KnnTcStats{};
   uint64_t* sc = nullptr;
+  uint32_t* self = nullptr;
   CAGRA_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sc), sizeof(uint64_t) * nq * K,
                                  stream));
-  launch_exact_topk_simt(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, nullptr, sc,
+  if (exclude_self && self_base) {
+    CAGRA_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&self), sizeof(uint32_t) * nq, stream));
+    iota_kernel<<<(nq + 255) / 256, 256, 0, stream>>>(self, nq, self_base);
+    CAGRA_LAUNCH_CHECK();
+  }
+  launch_exact_topk_simt(d_data, n, ld, d_queries, nq, qld, dim, K, exclude_self, self, sc,
                          d_ids, d_dists, stream);
   CAGRA_CUDA_TRY(cudaFreeAsync(sc, stream));
+  if (self) CAGRA_CUDA_TRY(cudaFreeAsync(self, stream));
 }
 
 }  // namespace cagra

@@ -242,6 +242,7 @@ struct TcArgs {
   uint32_t* bcount;     // mode 1: keys appended per row (> capg: overflow), zeroed by the host
   uint32_t capg;
   const uint32_t* self_ids;  // optional: data id of each query row (self exclusion)
+  uint32_t self_base;        // else: query row r is data point self_base + r
   const uint32_t* prow;      // TS: query-side rows (nq x Kp bf16, as Kp/2 u32) for TMEM
   uint32_t groups;           // CTAs start their sweep at one of `groups` evenly spaced tiles
 };
@@ -452,7 +453,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tau_f = key_dist(P.tau_keys[(size_t)row * P.tau_ld + P.tau_ld - 1]);
     uint32_t cnt = 0, gcnt = 0;
     // this row's own column in B coordinates (self exclusion), or none
-    const uint32_t self_id = live && P.self_ids ? P.self_ids[row] : row;
+    const uint32_t self_id = live && P.self_ids ? P.self_ids[row] : row + P.self_base;
     const uint32_t self_c = (P.exclude_self && self_id % P.col_stride == 0)
                                 ? self_id / P.col_stride
                                 : 0xffffffffu;
@@ -875,6 +876,12 @@ __global__ void gather_f32_kernel(const float* __restrict__ src, const uint32_t*
   if (i < cnt) dst[i] = src[rows[i]];
 }
 
+__global__ void offset_ids_kernel(const uint32_t* __restrict__ rows, uint32_t cnt, uint32_t base,
+                                  uint32_t* __restrict__ dst) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) dst[i] = rows[i] + base;
+}
+
 __global__ void gather_rows_kernel(const float* __restrict__ src, uint32_t ld,
                                    const uint32_t* __restrict__ rows, uint32_t cnt,
                                    float* __restrict__ dst) {
@@ -989,6 +996,7 @@ struct TcCall {
   const float* data;
   uint32_t n, ld, dim, K, Kp, kblocks, stages;
   bool exclude_self;
+  uint32_t self_base;  // kNN rows [self_base, self_base + nq) of the graph (row-sharded builds)
   float eps_rel, eps_norm;
   const uint32_t* maxnorm;
   const void* R;  // n x Kp bf16
@@ -1066,6 +1074,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   a.col_stride = 1;
   a.lists = lists.as<uint64_t>();
   a.self_ids = self_ids;
+  a.self_base = self_ids ? 0 : c.self_base;
   run_tc_kernel(c, P, tmA, tmB, a, nq);
   uint32_t* fail_cnt = fails.as<uint32_t>();
   uint32_t* fail_rows = fail_cnt + 1;
@@ -1093,6 +1102,11 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
           reinterpret_cast<const float*>(self_ids), fail_rows, nf, sid.as<float>());
       CAGRA_LAUNCH_CHECK();
       simt_self = sid.as<uint32_t>();
+    } else if (c.self_base) {
+      offset_ids_kernel<<<(nf + 255) / 256, 256, 0, c.stream>>>(fail_rows, nf, c.self_base,
+                                                                 sid.as<uint32_t>());
+      CAGRA_LAUNCH_CHECK();
+      simt_self = sid.as<uint32_t>();
     } else {
       simt_self = fail_rows;
     }
@@ -1112,9 +1126,10 @@ constexpr uint32_t kSampleStride = 16;
 
 void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
-                   uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
+                   uint32_t self_base, uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
   if (nq == 0) return;
   TcCall c;
+  c.self_base = exclude_self ? self_base : 0;
   c.data = d_data;
   c.n = n;
   c.ld = ld;
@@ -1135,8 +1150,10 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   c.eps_rel = 2.0f * 3.1f * 1.52587890625e-05f + 2.0f * (float)c.Kp * u23 + 4.0f * u23;
   c.eps_norm = (float)c.Kp * u23 + (float)(dim + 8) * u23 + 2.0f * u23;
 
-  const bool same = exclude_self;  // kNN graph: queries are the data rows
-  Dev dP((size_t)nq * c.Kp * 2), dR((size_t)n * c.Kp * 2), dqn(4ull * nq), dxn(4ull * n), dmax(4);
+  // kNN graph: the queries are data rows [self_base, self_base + nq), so the
+  // data split also yields their query-side rows
+  const bool same = exclude_self;
+  Dev dP((size_t)(same ? n : nq) * c.Kp * 2), dR((size_t)n * c.Kp * 2), dqn(4ull * nq), dxn(4ull * n), dmax(4);
   CAGRA_CUDA_TRY(cudaMemsetAsync(dmax.p, 0, 4, stream));
   Dev dmu(4ull * dim), dpart(8ull * kMeanChunks * dim);
   col_mean_partial_kernel<<<dim3((dim + 31) / 32, kMeanChunks), 256, 0, stream>>>(
@@ -1150,7 +1167,8 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
                                                    dR.as<__nv_bfloat16>(), dxn.as<float>(),
                                                    dmax.as<uint32_t>());
   CAGRA_LAUNCH_CHECK();
-  const float* qnorm = dxn.as<float>();
+  const float* qnorm = dxn.as<float>() + c.self_base;
+  const void* Pq = dP.as<uint16_t>() + (size_t)c.self_base * c.Kp;
   if (!same) {
     tc_split_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(d_queries, nq, qld, dim, c.Kp,
                                                       dmu.as<float>(), dP.as<__nv_bfloat16>(),
@@ -1166,7 +1184,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
   const char* onepass = std::getenv("CAGRA_TC_ONEPASS");
   const bool two_pass = n / kSampleStride >= 4096 && !(onepass && onepass[0] == '1');
   if (!two_pass) {
-    list_pass(c, dP.p, nq, qnorm, d_queries, qld, nullptr, d_ids, d_dists, reranked, fallback);
+    list_pass(c, Pq, nq, qnorm, d_queries, qld, nullptr, d_ids, d_dists, reranked, fallback);
   } else {
     // pass 1: every 16th point; the r-th smallest d~ over the sample is an
     // upper bound of the r-th smallest over all points (valid for ANY r).
@@ -1179,7 +1197,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
     CAGRA_CUDA_TRY(cudaMemsetAsync(bcount.p, 0, 4ull * nq, stream));  // append counters
     const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
-    CUtensorMap tmA = make_map(dP.p, nq, c.Kp, 1);
+    CUtensorMap tmA = make_map(Pq, nq, c.Kp, 1);
     CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride, brows);
     CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1, brows);
     TcArgs a{};
@@ -1188,7 +1206,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     a.mode = 0;
     a.col_stride = kSampleStride;
     a.lists = lists1.as<uint64_t>();
-    run_tc_kernel(c, dP.p, tmA, tmS, a, nq);
+    run_tc_kernel(c, Pq, tmA, tmS, a, nq);
     // pass 2: every point with d~ <= tau* appended (no merging)
     TcArgs b{};
     b.n = n;
@@ -1200,7 +1218,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     b.bufs = bufs.as<uint64_t>();
     b.bcount = bcount.as<uint32_t>();
     b.capg = capg;
-    run_tc_kernel(c, dP.p, tmA, tmB, b, nq);
+    run_tc_kernel(c, Pq, tmA, tmB, b, nq);
     uint32_t* fail_cnt = fails.as<uint32_t>();
     uint32_t* fail_rows = fail_cnt + 1;
     tc_rerank_append_kernel<<<(nq + 7) / 8, 256, 0, stream>>>(
@@ -1220,15 +1238,24 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       // mode on just those rows
       Dev P2((size_t)nf * c.Kp * 2), qn2(4ull * nf), q2((size_t)nf * qld * 4), ids2(4ull * nf * K),
           d2(4ull * nf * K);
-      gather_u16_rows_kernel<<<nf, 128, 0, stream>>>(dP.as<uint16_t>(), c.Kp, fail_rows, nf,
+      gather_u16_rows_kernel<<<nf, 128, 0, stream>>>(static_cast<const uint16_t*>(Pq), c.Kp,
+                                                     fail_rows, nf,
                                                      P2.as<uint16_t>());
       gather_f32_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(qnorm, fail_rows, nf,
                                                               qn2.as<float>());
       gather_rows_kernel<<<nf, 128, 0, stream>>>(d_queries, qld, fail_rows, nf, q2.as<float>());
       CAGRA_LAUNCH_CHECK();
-      list_pass(c, P2.p, nf, qn2.as<float>(), q2.as<float>(), qld,
-                exclude_self ? fail_rows : nullptr, ids2.as<uint32_t>(), d2.as<float>(), reranked,
-                fallback);
+      // the retried rows' data ids (their self columns)
+      Dev sid2(4ull * nf);
+      const uint32_t* self2 = nullptr;
+      if (exclude_self) {
+        offset_ids_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(fail_rows, nf, c.self_base,
+                                                                sid2.as<uint32_t>());
+        CAGRA_LAUNCH_CHECK();
+        self2 = sid2.as<uint32_t>();
+      }
+      list_pass(c, P2.p, nf, qn2.as<float>(), q2.as<float>(), qld, self2, ids2.as<uint32_t>(),
+                d2.as<float>(), reranked, fallback);
       scatter_rows_kernel<<<nf, 128, 0, stream>>>(fail_rows, nf, K, ids2.as<uint32_t>(),
                                                   d2.as<float>(), d_ids, d_dists);
       CAGRA_LAUNCH_CHECK();

@@ -1042,8 +1042,9 @@ team_merge_kernel(const unsigned long long* __restrict__ team_out,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t total = T * M, P2 = max(256u, next_pow2_u32(total));
+  const uint32_t F = max(256u, next_pow2_u32(k));             // k <= M may exceed 256
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);   // P2
-  uint64_t* fin = keys + P2;                                  // 256
+  uint64_t* fin = keys + P2;                                  // F
   __shared__ uint32_t nfin;
   for (uint32_t i = tid; i < P2; i += SNT)
     keys[i] = i < total ? cmp_key(team_out[(size_t)q * total + i]) : kDummyKey;
@@ -1067,7 +1068,7 @@ team_merge_kernel(const unsigned long long* __restrict__ team_out,
     // sequential-chain re-score: each warp stages a candidate row and the
     // query in shared memory with coalesced loads, then one lane runs the
     // chain from smem (a per-dimension dependent global load would dominate)
-    float* rowbuf = reinterpret_cast<float*>(fin + 256) + warp * 2 * ld;
+    float* rowbuf = reinterpret_cast<float*>(fin + F) + warp * 2 * ld;
     const float* qv = queries + (size_t)q * ld;
     for (uint32_t i = warp; i < live; i += SNT / 32) {
       const uint32_t id = key_id(fin[i]);
@@ -1085,7 +1086,13 @@ team_merge_kernel(const unsigned long long* __restrict__ team_out,
       __syncwarp();
     }
     __syncthreads();
-    if (warp == 0) warp_sort_smem(fin, live, lane);
+    if (live <= 256) {
+      if (warp == 0) warp_sort_smem(fin, live, lane);
+    } else {
+      for (uint32_t j = live + tid; j < F; j += SNT) fin[j] = kDummyKey;
+      __syncthreads();
+      block_sort_any(fin, F);
+    }
     __syncthreads();
   }
   for (uint32_t i = tid; i < k; i += SNT) {
@@ -1483,6 +1490,15 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
     throw UsageErr("batch_search: lockstep shared mode supports 2 <= team_count <= 16");
   if (pl.mc && (T < 2 || T > 256))
     throw UsageErr("batch_search: multi-CTA shared mode supports 2 <= team_count <= 256");
+  if (pl.mc) {
+    // K7 stages the union of the team lists (T*M keys), the k finalists and
+    // one row pair per warp in shared memory (launch_search)
+    const uint64_t msmem = 8ull * (std::max<uint64_t>(256, next_pow2_u32(T * c.topm)) +
+                                   std::max<uint32_t>(256, next_pow2_u32(c.k))) +
+                           8ull * ix.ld * (SNT / 32);
+    if (msmem > 200 * 1024)
+      throw UsageErr("search: team_count * M exceeds the team-merge shared-memory budget");
+  }
   const uint32_t p = shared_mode ? 1 : c.width;
   const uint32_t d = ix.degree;
   const uint32_t C = p * d;
@@ -1632,7 +1648,8 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   if (pl.mc) {
     const uint32_t total = pl.teams * c.topm;
     const uint32_t P2 = std::max(256u, next_pow2_u32(total));
-    const size_t msmem = 8ull * (P2 + 256) + sizeof(float) * 2 * ix.ld * (SNT / 32);
+    const uint32_t F = std::max(256u, next_pow2_u32(c.k));
+    const size_t msmem = 8ull * (P2 + F) + sizeof(float) * 2 * ix.ld * (SNT / 32);
     CAGRA_CUDA_TRY(cudaFuncSetAttribute(team_merge_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
     team_merge_kernel<<<nq, SNT, msmem, stream>>>(

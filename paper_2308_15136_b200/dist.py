@@ -91,24 +91,37 @@ class ShardedIndex:
         return cls(data_shard, g, offset, device)
 
     def search_local(self, d_queries, nq: int, params: fodg.SearchParams,
-                     opts: Optional[fodg.EngineOptions] = None, stream: int = 0):
-        """Per-shard search of device-resident queries (row stride = index.ld)."""
+                     opts: Optional[fodg.EngineOptions] = None, stream: Optional[int] = None):
+        """Per-shard search of device-resident queries (row stride = index.ld),
+        asynchronous on `stream` (default: torch's current stream on this
+        device, so torch/NCCL work queued after it is ordered after the search)."""
         import torch
 
         opts = opts or fodg.EngineOptions(device=self.device)
         dev = torch.device("cuda", self.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
         ids = torch.empty((nq, params.k), dtype=torch.int32, device=dev)
         dists = torch.empty((nq, params.k), dtype=torch.float32, device=dev)
         self.index.search_dev(d_queries, nq, params, opts, ids, dists, None, None, stream)
         return ids, dists
 
     def search(self, d_queries, nq: int, params: fodg.SearchParams, offsets: List[int],
-               opts: Optional[fodg.EngineOptions] = None, group=None, stream: int = 0):
+               opts: Optional[fodg.EngineOptions] = None, group=None):
         """Global top-k for every query on every rank: local search, one
-        all-gather of the per-shard lists, K8 merge."""
+        all-gather of the per-shard lists, K8 merge.  Everything is queued on
+        torch's current stream: with NCCL the all-gather is stream-ordered after
+        the search (no host sync); with gloo (CPU tensors) the copy to the host
+        synchronises first."""
         import torch
+        import torch.distributed as dist
 
+        dev = torch.device("cuda", self.device)
+        stream = torch.cuda.current_stream(dev).cuda_stream
         ids, dists = self.search_local(d_queries, nq, params, opts, stream)
-        torch.cuda.current_stream(self.device).synchronize()
-        gi, gd = exchange_topk(ids, dists, group)
+        if dist.get_backend(group) == "nccl":
+            gi, gd = exchange_topk(ids, dists, group)
+        else:
+            gi, gd = exchange_topk(ids.cpu(), dists.cpu(), group)
+            gi, gd = gi.to(dev), gd.to(dev)
         return merge_shard_topk(gi, gd, offsets, self.device, stream)

@@ -2,12 +2,17 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <list>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
+
+#include "fodg/b200.hpp"
 
 namespace fodg::b200 {
 
@@ -25,6 +30,24 @@ void check(int rc) {
 int device() {
     const char* e = std::getenv("CAGRA_DEVICE");
     return e ? std::atoi(e) : 0;
+}
+
+std::vector<int> devices() {
+    // CAGRA_DEVICES=0,1,2,3 spreads batch_search / exact_knn_graph over those
+    // GPUs (query-sharded replicas, row-sharded kNN build); default: device()
+    std::vector<int> out;
+    if (const char* e = std::getenv("CAGRA_DEVICES")) {
+        const char* s = e;
+        while (*s) {
+            char* end = nullptr;
+            const long v = std::strtol(s, &end, 10);
+            if (end == s) break;
+            out.push_back(static_cast<int>(v));
+            s = *end == ',' ? end + 1 : end;
+        }
+    }
+    if (out.empty()) out.push_back(device());
+    return out;
 }
 
 bool fast_distances() {
@@ -46,46 +69,84 @@ unsigned device_sm_count() {
 
 namespace {
 
-// FNV-1a over the whole buffer when small, else over 4096 evenly spaced
-// 64-byte windows: detects a rebuilt or edited index at the same address.
-std::uint64_t fingerprint(const void* p, std::size_t bytes) {
-    const auto* b = static_cast<const unsigned char*>(p);
-    std::uint64_t h = 1469598103934665603ull;
-    auto eat = [&](std::size_t lo, std::size_t hi) {
-        for (std::size_t i = lo; i < hi; ++i) h = (h ^ b[i]) * 1099511628211ull;
-    };
-    if (bytes <= (64u << 20)) {
-        eat(0, bytes);
-    } else {
-        const std::size_t step = bytes / 4096;
-        for (std::size_t w = 0; w < 4096; ++w) eat(w * step, w * step + 64);
-        eat(bytes - 64, bytes);
+// ---- content hash ----------------------------------------------------------
+// The reference reads its `const Graph&, const Dataset&` afresh on every call,
+// so the device copy may be reused only while the host contents are exactly
+// the ones uploaded.  Every cached lookup therefore hashes the WHOLE of both
+// buffers (no sampling): four independent 64-bit multiply-rotate lanes per
+// chunk, chunks spread over host threads for large buffers (memory-bound,
+// tens of GB/s), folded in chunk order so the value is thread-count independent.
+inline std::uint64_t rotl(std::uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+std::uint64_t hash_chunk(const unsigned char* p, std::size_t bytes, std::uint64_t seed) {
+    constexpr std::uint64_t P1 = 0x9e3779b185ebca87ull, P2 = 0xc2b2ae3d27d4eb4full;
+    std::uint64_t a = seed ^ P1, b = seed ^ P2, c = seed + P1, d = seed - P2;
+    std::size_t i = 0;
+    for (; i + 32 <= bytes; i += 32) {
+        std::uint64_t w[4];
+        std::memcpy(w, p + i, 32);
+        a = rotl(a ^ (w[0] * P2), 31) * P1;
+        b = rotl(b ^ (w[1] * P2), 31) * P1;
+        c = rotl(c ^ (w[2] * P2), 31) * P1;
+        d = rotl(d ^ (w[3] * P2), 31) * P1;
     }
-    return h ^ bytes;
+    std::uint64_t h = rotl(a, 1) + rotl(b, 7) + rotl(c, 12) + rotl(d, 18);
+    for (; i < bytes; ++i) h = (h ^ p[i]) * P1;
+    return (h ^ (h >> 29)) * P2 ^ bytes;
 }
 
-struct Entry {
+std::uint64_t content_hash(const void* p, std::size_t bytes) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    constexpr std::size_t kChunk = 8u << 20;
+    const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
+    if (chunks <= 1) return hash_chunk(b, bytes, 0x5eed);
+    std::vector<std::uint64_t> part(chunks);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = static_cast<unsigned>(std::min<std::size_t>(hw, chunks));
+    auto work = [&](unsigned t) {
+        for (std::size_t c = t; c < chunks; c += nt) {
+            const std::size_t lo = c * kChunk, len = std::min(kChunk, bytes - lo);
+            part[c] = hash_chunk(b + lo, len, c);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    return hash_chunk(reinterpret_cast<const unsigned char*>(part.data()), 8 * chunks, bytes);
+}
+
+bool trust_identity() {
+    // CAGRA_INDEX_CACHE=identity: the caller promises not to mutate a searched
+    // Graph/Dataset in place (or calls invalidate_index_cache() after doing so);
+    // lookups then match on addresses and shapes only and skip the hash
+    const char* e = std::getenv("CAGRA_INDEX_CACHE");
+    return e && std::strcmp(e, "identity") == 0;
+}
+
+struct CacheEntry {
     const void* data;
     const void* ids;
     std::uint32_t n, dim, degree;
-    std::uint64_t fp_data, fp_ids;
+    std::uint64_t h_data, h_ids;
     cagra_index* ix;
 };
 
 std::mutex g_mu;
-std::list<Entry> g_cache;  // most recent first
+std::list<CacheEntry> g_cache;  // most recent first
 constexpr std::size_t kMaxCached = 4;
 
 }  // namespace
 
 cagra_index* index_for(const Graph& graph, const Dataset& ds) {
-    const std::uint64_t fd = fingerprint(ds.raw(), 4ull * ds.size() * ds.dim());
-    const std::uint64_t fi = fingerprint(graph.ids.data(), 4ull * graph.ids.size());
+    const bool identity = trust_identity();
+    const std::uint64_t hd = identity ? 0 : content_hash(ds.raw(), 4ull * ds.size() * ds.dim());
+    const std::uint64_t hi = identity ? 0 : content_hash(graph.ids.data(), 4ull * graph.ids.size());
     std::lock_guard<std::mutex> lock(g_mu);
     for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
         if (it->data == ds.raw() && it->ids == graph.ids.data() && it->n == ds.size() &&
-            it->dim == ds.dim() && it->degree == graph.degree && it->fp_data == fd &&
-            it->fp_ids == fi) {
+            it->dim == ds.dim() && it->degree == graph.degree &&
+            (identity || (it->h_data == hd && it->h_ids == hi))) {
             g_cache.splice(g_cache.begin(), g_cache, it);
             return it->ix;
         }
@@ -93,12 +154,20 @@ cagra_index* index_for(const Graph& graph, const Dataset& ds) {
     cagra_index* ix = nullptr;
     check(cagra_index_create(ds.raw(), ds.size(), ds.dim(), graph.ids.data(), graph.degree,
                              device(), &ix));
-    g_cache.push_front({ds.raw(), graph.ids.data(), ds.size(), ds.dim(), graph.degree, fd, fi, ix});
+    g_cache.push_front({ds.raw(), graph.ids.data(), ds.size(), ds.dim(), graph.degree, hd, hi, ix});
     while (g_cache.size() > kMaxCached) {
         cagra_index_destroy(g_cache.back().ix);
         g_cache.pop_back();
     }
     return ix;
 }
+
+void invalidate_index_cache() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (auto& e : g_cache) cagra_index_destroy(e.ix);
+    g_cache.clear();
+}
+
+std::uint64_t host_content_hash(const void* p, std::size_t bytes) { return content_hash(p, bytes); }
 
 }  // namespace fodg::b200

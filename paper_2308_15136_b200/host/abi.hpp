@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "cagra/capi.h"
 #include "fodg/dataset.hpp"
@@ -19,6 +20,10 @@ void check(int rc);
 
 /// CUDA device used by the drop-in (env CAGRA_DEVICE, default 0).
 int device();
+
+/// Devices the drop-in spreads batch_search / exact_knn_graph over
+/// (env CAGRA_DEVICES=0,1,..., default {device()}).
+std::vector<int> devices();
 
 /// Fast in-loop distances (team reductions; reported distances still the
 /// sequential chain) instead of the reference-order chain everywhere.  Off by
