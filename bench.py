@@ -296,12 +296,15 @@ def run_ours(args):
         g, binfo = fodg.build_graph(ds, args.degree, device=local)
     build_wall = time.perf_counter() - t0
     kst = capi.knn_last_stats()
-    kp = -(-(3 * args.dim + 6) // 64) * 64
-    # bf16 tensor-core work of the kNN build: sample pass (1/16) + full pass,
-    # 2*N*N*Kp each (Kp = 3*dim + 6 padded to 64: bf16x3 split + folded norms)
-    tc_flops = 2.0 * args.n * args.n * kp * (1 + 1 / 16)
+    # tensor work of the kNN build: sample pass (every 16th point) + full
+    # pass, 2*N*N*K each, K = the filter GEMM's K (fp16 single term: dim + 2
+    # rounded to 16; bf16x3: 3*dim + 6)
+    gk = kst["gemm_k"]
+    tc_flops = 2.0 * args.n * args.n * gk * (1 + 1 / 16)
     tc = kst["rows"] > 0  # 0 rows: the SIMT sequential-chain kernel ran (dim too large)
-    knn_stats = {"path": ("tcgen05 bf16x3 GEMM + exact re-rank (bit-exact)" if tc else
+    split = {1: "fp16 single-term", 3: "bf16x3"}.get(kst["split_terms"], "?")
+    knn_stats = {"path": (f"tcgen05 {split} filter GEMM (K={gk}) + exact re-rank (bit-exact)"
+                          if tc else
                           "SIMT sequential-chain fp32 (bit-exact; dim beyond the tensor-core path)"),
                  "tensor_tflops": tc_flops / binfo["knn_seconds"] / 1e12 if tc else None,
                  "fp32_equiv_tflops": 2.0 * args.n * args.n * args.dim / binfo["knn_seconds"] / 1e12,

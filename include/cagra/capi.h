@@ -147,6 +147,16 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
 int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked,
                          uint64_t* retried_rows);
 
+/* Filter of the last tensor-core kNN / top-k call: split_terms 1 = fp16
+ * single term, 3 = bf16x3; gemm_k = K of the filter GEMM (MMA work per
+ * (query, point) pair = 2 gemm_k flops).  Either pointer may be NULL. */
+int cagra_knn_last_filter(uint32_t* split_terms, uint32_t* gemm_k);
+
+/* The kNN build keeps its large scratch (16-bit operand rows, candidate
+ * buffers) cached per device between calls; this releases it (device < 0: all
+ * devices).  No reference counterpart (the reference allocates per call). */
+int cagra_trim_scratch(int device);
+
 /* ---- graph quality metrics ----------------------------------------------- */
 /* strong_cc_count (graph_metrics.hpp:22) and the integer total behind
  * avg_2hop_count (graph_metrics.hpp:26; mean = two_hop_total / n), on the

@@ -88,7 +88,7 @@ EXPORTS = [
     "cagra_optimize", "cagra_build_graph", "cagra_index_create", "cagra_index_create_dev",
     "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
     "cagra_search_dev", "cagra_last_launch_count", "cagra_merge_shard_topk_dev",
-    "cagra_graph_metrics",
+    "cagra_graph_metrics", "cagra_trim_scratch", "cagra_knn_last_filter",
 ]
 
 _lib = None
@@ -163,7 +163,10 @@ def knn_last_stats() -> dict:
     reranked); all zero when the SIMT path ran."""
     v = (C.c_uint64 * 4)()
     lib().cagra_knn_last_stats(C.byref(v, 0), C.byref(v, 8), C.byref(v, 16), C.byref(v, 24))
-    return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2], "retried_rows": v[3]}
+    f = (C.c_uint32 * 2)()
+    lib().cagra_knn_last_filter(C.byref(f, 0), C.byref(f, 4))
+    return {"rows": v[0], "fallback_rows": v[1], "reranked": v[2], "retried_rows": v[3],
+            "split_terms": f[0], "gemm_k": f[1]}
 
 
 def graph_metrics(graph: np.ndarray, device: int = 0):

@@ -159,7 +159,11 @@ void optimize_device(const uint32_t* d_knn, const float* d_dists, uint32_t n, ui
   if (hflag & 2) throw UsageErr("optimize: neighbour id out of range");
   if (hflag & 1) throw UsageErr("graph_opt: input rows must be distance-sorted");
   Event e0, e1, e2, e3, e4;
+  // every scratch buffer is allocated before the first event, so the stage
+  // times are device time, not host allocation time
   DBuf pruned(sizeof(uint32_t) * (size_t)n * d);
+  DBuf scratch(add_reverse ? reverse_scratch_bytes(n, d) : 0);
+  DBuf rc(add_reverse ? sizeof(uint32_t) * n : 0), ri(add_reverse ? sizeof(uint32_t) * (size_t)n * d : 0);
   CAGRA_CUDA_TRY(cudaEventRecord(e0.e, s));
   if (reorder) {
     launch_detour_reorder(d_knn, n, deg, d, nullptr, pruned.as<uint32_t>(), s);
@@ -169,8 +173,6 @@ void optimize_device(const uint32_t* d_knn, const float* d_dists, uint32_t n, ui
   }
   CAGRA_CUDA_TRY(cudaEventRecord(e1.e, s));
   if (add_reverse) {
-    DBuf scratch(reverse_scratch_bytes(n, d));
-    DBuf rc(sizeof(uint32_t) * n), ri(sizeof(uint32_t) * (size_t)n * d);
     launch_reverse(pruned.as<uint32_t>(), n, d, d, scratch.p, rc.as<uint32_t>(), ri.as<uint32_t>(),
                    s);
     CAGRA_CUDA_TRY(cudaEventRecord(e2.e, s));
@@ -479,6 +481,16 @@ int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* q
                                    cudaMemcpyDeviceToHost, st.s));
     st.sync();
   });
+}
+
+int cagra_knn_last_filter(uint32_t* split_terms, uint32_t* gemm_k) {
+  if (split_terms) *split_terms = g_knn_tc_stats.split_terms;
+  if (gemm_k) *gemm_k = g_knn_tc_stats.gemm_k;
+  return CAGRA_OK;
+}
+
+int cagra_trim_scratch(int device) {
+  return guarded([&] { knn_trim_scratch(device); });
 }
 
 int cagra_knn_last_stats(uint64_t* rows, uint64_t* fallback_rows, uint64_t* reranked,

@@ -25,15 +25,19 @@ void launch_exact_topk_simt(const float* d_data, uint32_t n, uint32_t ld, const 
                             bool exclude_self, const uint32_t* d_self_ids,
                             uint64_t* d_topk_scratch, uint32_t* d_ids, float* d_dists,
                             cudaStream_t stream);
-// tcgen05 path (bf16x3 split GEMM + heap top-(K+32) + exact re-rank); synchronous.
+// tcgen05 path (fp16 single-term or bf16x3 split GEMM filter + exact re-rank); synchronous.
 bool knn_tc_eligible(uint32_t dim, uint32_t K);
 void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_queries,
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
                    uint32_t self_base, uint32_t* d_ids, float* d_dists, cudaStream_t stream);
 struct KnnTcStats {
   uint64_t rows = 0, fallback_rows = 0, reranked = 0, retried_rows = 0;
+  uint32_t split_terms = 0;  // filter split of the last call: 1 fp16, 3 bf16x3
+  uint32_t gemm_k = 0;       // K of the filter GEMM (16-wide MMA steps actually issued)
 };
 extern KnnTcStats g_knn_tc_stats;
+// Frees the kNN build's cached scratch on `device` (all devices when < 0).
+void knn_trim_scratch(int device);
 
 // ---- metrics.cu ---------------------------------------------------------------
 // Distinct <=2-hop neighbours summed over all nodes (avg_2hop_count * n) and

@@ -75,19 +75,22 @@ def test_knn_odd_dimension_and_ragged_tiles(gpu, oracle):
         assert np.array_equal(bits(knn.dists), bits(ref_d))
 
 
+@pytest.mark.parametrize("split", ["1", "3"])
 @pytest.mark.parametrize("n,dim,k,two_pass", [
-    (3000, 128, 64, False),    # single pass, D=128 (7 K-blocks, 3-stage ring)
+    (3000, 128, 64, False),    # single pass, D=128
     (70000, 96, 128, True),    # sample pass + append pass (DEEP shape, d_init 128)
     (90000, 37, 40, True),     # odd dim, ragged last tile
-    (4000, 200, 32, False),    # K = 640 > 512: query tile streamed with each data tile
+    (4000, 200, 32, False),    # K > 512 (bf16x3): query tile streamed with each data tile
     (70000, 960, 128, True),   # GIST shape, streamed query tile, both passes
 ])
-def test_knn_tensor_core_path_bit_exact(gpu, oracle, monkeypatch, n, dim, k, two_pass):
+def test_knn_tensor_core_path_bit_exact(gpu, oracle, monkeypatch, n, dim, k, two_pass, split):
     # K1 on tcgen05 (knn_tc.cu) against the SIMT sequential-chain kernel (itself
-    # bit-exact vs the reference above) and, on the small case, the oracle.
+    # bit-exact vs the reference above) and, on the small case, the oracle;
+    # both filter splits (fp16 single term, bf16x3).
     data = oracle.uniform_dataset(n, dim, 1000 + n)
     ds = fodg.Dataset.from_array(data)
     monkeypatch.setenv("CAGRA_KNN_PATH", "auto")
+    monkeypatch.setenv("CAGRA_KNN_SPLIT", split)
     tc = fodg.exact_knn_graph(ds, k)
     st = capi.knn_last_stats()
     assert st["rows"] == n and st["reranked"] >= n * k, st   # the tensor-core path ran
@@ -105,6 +108,25 @@ def test_knn_tensor_core_path_bit_exact(gpu, oracle, monkeypatch, n, dim, k, two
         ref_ids, ref_d = oracle.exact_knn_graph(data, k)
         assert np.array_equal(tc.ids, ref_ids)
         assert np.array_equal(bits(tc.dists), bits(ref_d))
+
+
+@pytest.mark.parametrize("scale,offset", [(1e6, 3e7), (1e-12, 0.0), (1e-18, 0.0), (1.0, -250.0)])
+def test_knn_tensor_core_extreme_magnitudes(gpu, oracle, monkeypatch, scale, offset):
+    # the fp16 split scales rows by a power of two chosen from the largest
+    # centred norm: huge, tiny and offset data stay bit-exact (the error
+    # bound covers fp16 rounding and subnormal operands)
+    base = oracle.uniform_dataset(70000, 48, 31)
+    data = np.ascontiguousarray((base * np.float32(scale) + np.float32(offset)).astype(np.float32))
+    # a few rows far from the rest (large centred norms next to small ones)
+    data[::9973] *= np.float32(3.0)
+    ds = fodg.Dataset.from_array(data)
+    monkeypatch.setenv("CAGRA_KNN_PATH", "auto")
+    tc = fodg.exact_knn_graph(ds, 24)
+    assert capi.knn_last_stats()["rows"] == 70000
+    monkeypatch.setenv("CAGRA_KNN_PATH", "simt")
+    simt = fodg.exact_knn_graph(ds, 24)
+    assert np.array_equal(tc.ids, simt.ids)
+    assert np.array_equal(bits(tc.dists), bits(simt.dists))
 
 
 def test_knn_tensor_core_single_pass_forced(gpu, oracle, monkeypatch):
