@@ -47,6 +47,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -1077,11 +1078,30 @@ __global__ void scatter_rows_kernel(const uint32_t* __restrict__ rows, uint32_t 
 // ------------------------------------------------------------ host side ----
 // Scratch of one kNN call.  (A stream-ordered pool was measured slower for
 // the first, cold build — the one a graph build pays — so plain cudaMalloc.)
+// Stream-ordered scratch of the occasional paths (small-batch list pass,
+// retried rows): cudaMallocAsync from the device pool, whose release threshold
+// is raised once so freed blocks stay mapped — a plain cudaMalloc/cudaFree
+// pair here was measured stalling the host for up to ~350 ms between passes.
+void keep_pool_mapped() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || done[dev & 63]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev & 63] = true;
+}
 struct Dev {
   void* p = nullptr;
-  explicit Dev(size_t b) { CAGRA_CUDA_TRY(cudaMalloc(&p, b ? b : 16)); }
+  cudaStream_t s = nullptr;
+  Dev(size_t b, cudaStream_t st) : s(st) {
+    keep_pool_mapped();
+    CAGRA_CUDA_TRY(cudaMallocAsync(&p, b ? b : 16, s));
+  }
   ~Dev() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
@@ -1235,6 +1255,42 @@ bool knn_tc_eligible(uint32_t dim, uint32_t K) {
 
 namespace {
 
+// CAGRA_KNN_TRACE=1: device-event and host-wall time of every build phase to
+// stderr (diagnostics for the build-time spread across runs).
+struct Tracer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> wall;
+  std::chrono::steady_clock::time_point t0;
+  explicit Tracer(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("CAGRA_KNN_TRACE");
+    on = e && e[0] == '1';
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+    wall.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
+  }
+  ~Tracer() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    std::fprintf(stderr, "[knn trace]");
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      std::fprintf(stderr, " %s %.2fms(host %.1f)", ev[i].first, ms, wall[i]);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto& p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 // Everything one kNN / top-k call shares between its passes.
 struct TcCall {
   const float* data;
@@ -1334,7 +1390,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
                         : std::min<uint32_t>((2u * (uint32_t)sms + row_ctas - 1) / row_ctas,
                                              std::max<uint32_t>(1, ntiles / 8));
   if (std::getenv("CAGRA_TC_NOSPLIT")) splits = 1;
-  Dev lists(8ull * nq * KC * splits), fails(4ull * nq + 4), rer(8);
+  Dev lists(8ull * nq * KC * splits, c.stream), fails(4ull * nq + 4, c.stream), rer(8, c.stream);
   CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, c.stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, c.stream));
   const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
@@ -1356,7 +1412,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
     const uint32_t m = std::max<uint32_t>(2, 1024 / KC);
     uint32_t g = splits;
     uint64_t* src = lists.as<uint64_t>();
-    Dev tmp(8ull * nq * KC * ((splits + m - 1) / m));
+    Dev tmp(8ull * nq * KC * ((splits + m - 1) / m), c.stream);
     uint64_t* dst = tmp.as<uint64_t>();
     while (g > 1) {
       const uint32_t go = (g + m - 1) / m;
@@ -1384,8 +1440,8 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   fallback += nf;
   if (!nf) return;
   // exact SIMT kernel for the rows whose candidate band overflowed
-  Dev q((size_t)nf * qld * 4), sid(4ull * nf), sc(8ull * nf * c.K), fi(4ull * nf * c.K),
-      fd(4ull * nf * c.K);
+  Dev q((size_t)nf * qld * 4, c.stream), sid(4ull * nf, c.stream), sc(8ull * nf * c.K, c.stream),
+      fi(4ull * nf * c.K, c.stream), fd(4ull * nf * c.K, c.stream);
   gather_rows_kernel<<<nf, 128, 0, c.stream>>>(queries, qld, fail_rows, nf, q.as<float>());
   CAGRA_LAUNCH_CHECK();
   const uint32_t* simt_self = nullptr;
@@ -1422,6 +1478,8 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
                    uint32_t self_base, uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
   if (nq == 0) return;
   std::lock_guard<std::mutex> lk(g_knn_mu);
+  Tracer tr(stream);
+  tr.mark("start");
   TcCall c;
   c.self_base = exclude_self ? self_base : 0;
   c.data = d_data;
@@ -1539,6 +1597,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
     std::memcpy(&c.xm, &hm, 4);
   }
+  tr.mark("prep");
   const float* qnorm_all = same ? dxn.as<float>() + c.self_base : dqn.as<float>();
   const uint16_t* Pq_all = dP.as<uint16_t>() + (same ? (size_t)c.self_base * c.Kp : 0);
   c.R = dR.p;
@@ -1599,7 +1658,9 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       a.lists = lists1.as<uint64_t>();
       a.self_base = cc.self_base;
       a.qnorm = f16 ? qnorm : nullptr;
+      tr.mark("setup");
       run_tc_kernel(cc, Pq, tmA, tmS, a, cq);
+      tr.mark("sample");
       // pass 2: every point with d~ <= tau* appended (no merging)
       TcArgs b{};
       b.n = n;
@@ -1614,6 +1675,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       b.self_base = cc.self_base;
       b.qnorm = a.qnorm;
       run_tc_kernel(cc, Pq, tmA, tmB, b, cq);
+      tr.mark("full");
       uint32_t* fail_cnt = fails.as<uint32_t>();
       uint32_t* fail_rows = fail_cnt + 1;
       tc_rerank_append_kernel<<<(cq + 7) / 8, 256, 0, stream>>>(
@@ -1628,18 +1690,19 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
       reranked += nre;
       retried += nf;
+      tr.mark("rerank");
       if (!nf) continue;
       // the rows whose threshold did not bracket their band: single-pass list
       // mode on just those rows
-      Dev P2((size_t)nf * c.Kp * 2), qn2(4ull * nf), q2((size_t)nf * qld * 4),
-          ids2(4ull * nf * K), d2(4ull * nf * K);
+      Dev P2((size_t)nf * c.Kp * 2, stream), qn2(4ull * nf, stream),
+          q2((size_t)nf * qld * 4, stream), ids2(4ull * nf * K, stream), d2(4ull * nf * K, stream);
       gather_u16_rows_kernel<<<nf, 128, 0, stream>>>(Pq, c.Kp, fail_rows, nf, P2.as<uint16_t>());
       gather_f32_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(qnorm, fail_rows, nf,
                                                               qn2.as<float>());
       gather_rows_kernel<<<nf, 128, 0, stream>>>(cqueries, qld, fail_rows, nf, q2.as<float>());
       CAGRA_LAUNCH_CHECK();
       // the retried rows' data ids (their self columns)
-      Dev sid2(4ull * nf);
+      Dev sid2(4ull * nf, stream);
       const uint32_t* self2 = nullptr;
       if (exclude_self) {
         offset_ids_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(fail_rows, nf, cc.self_base,
@@ -1655,6 +1718,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       CAGRA_CUDA_TRY(cudaStreamSynchronize(stream));
     }
   }
+  tr.mark("retry/end");
   g_knn_tc_stats.rows = nq;
   g_knn_tc_stats.fallback_rows = fallback;
   g_knn_tc_stats.reranked = reranked;

@@ -83,18 +83,23 @@ class ShardedIndex:
         self.offset = int(offset)
         self.device = device
         self.index = fodg.Index(fodg.Dataset.from_array(data_shard), graph, device)
+        self.build_info = {"knn_seconds": 0.0, "optimize_seconds": 0.0}
 
     @classmethod
     def build(cls, data_shard: np.ndarray, offset: int, degree: int, device: int = 0):
         ds = fodg.Dataset.from_array(data_shard)
-        g, _ = fodg.build_graph(ds, degree, device=device)
-        return cls(data_shard, g, offset, device)
+        g, info = fodg.build_graph(ds, degree, device=device)
+        sh = cls(data_shard, g, offset, device)
+        sh.build_info = info
+        return sh
 
     def search_local(self, d_queries, nq: int, params: fodg.SearchParams,
-                     opts: Optional[fodg.EngineOptions] = None, stream: Optional[int] = None):
+                     opts: Optional[fodg.EngineOptions] = None, stream: Optional[int] = None,
+                     stats=None):
         """Per-shard search of device-resident queries (row stride = index.ld),
         asynchronous on `stream` (default: torch's current stream on this
-        device, so torch/NCCL work queued after it is ordered after the search)."""
+        device, so torch/NCCL work queued after it is ordered after the search).
+        `stats`: optional [nq, 6] int32 device tensor for the per-query counters."""
         import torch
 
         opts = opts or fodg.EngineOptions(device=self.device)
@@ -103,7 +108,7 @@ class ShardedIndex:
             stream = torch.cuda.current_stream(dev).cuda_stream
         ids = torch.empty((nq, params.k), dtype=torch.int32, device=dev)
         dists = torch.empty((nq, params.k), dtype=torch.float32, device=dev)
-        self.index.search_dev(d_queries, nq, params, opts, ids, dists, None, None, stream)
+        self.index.search_dev(d_queries, nq, params, opts, ids, dists, None, stats, stream)
         return ids, dists
 
     def search(self, d_queries, nq: int, params: fodg.SearchParams, offsets: List[int],

@@ -134,3 +134,65 @@ def test_query_sharding_matches_single_gpu(gpu, oracle):
         s, e = pdist.query_slice(nq, 3, r)
         parts.append(ix.search(queries[s:e], prm, query_offset=s)[0])
     assert np.array_equal(np.concatenate(parts), full)
+
+
+def _sharded_search_worker(rank, world, port, out):
+    """One rank of a dataset-sharded index on the (shared) GPU, gloo exchange."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2308_15136_b200 import capi
+
+        n, dim, nq = 20000, 24, 300
+        data = capi.uniform_dataset(n, dim, 41)
+        queries = capi.uniform_dataset(nq, dim, 42)
+        bounds = pdist.shard_bounds(n, world)
+        s, e = bounds[rank]
+        sh = pdist.ShardedIndex.build(np.ascontiguousarray(data[s:e]), s, 16)
+        qd = torch.zeros((nq, sh.index.ld), dtype=torch.float32, device="cuda:0")
+        qd[:, :dim] = torch.from_numpy(queries).cuda()
+        prm = fodg.SearchParams(k=10, topm=64, width=2, seed=5)
+        mi, md = sh.search(qd, nq, prm, [b[0] for b in bounds])
+        torch.cuda.synchronize()
+        out[rank] = (mi.cpu().numpy().copy(), md.cpu().numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_index_search_world2_matches_one_process(gpu, oracle):
+    # ShardedIndex.search end to end over 2 ranks (gloo all-gather, K8 merge)
+    # equals the same shards searched and merged in one process, and reaches
+    # the global ground truth
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_sharded_search_worker, args=(world, _free_port(), out), nprocs=world,
+                 join=True)
+        res = dict(out)
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    from paper_2308_15136_b200 import capi
+
+    n, dim, nq = 20000, 24, 300
+    data = capi.uniform_dataset(n, dim, 41)
+    queries = capi.uniform_dataset(nq, dim, 42)
+    bounds = pdist.shard_bounds(n, world)
+    prm = fodg.SearchParams(k=10, topm=64, width=2, seed=5)
+    li, ld_ = [], []
+    for s, e in bounds:
+        sh = pdist.ShardedIndex.build(np.ascontiguousarray(data[s:e]), s, 16)
+        qd = torch.zeros((nq, sh.index.ld), dtype=torch.float32, device="cuda:0")
+        qd[:, :dim] = torch.from_numpy(queries).cuda()
+        i, d = sh.search_local(qd, nq, prm)
+        li.append(i)
+        ld_.append(d)
+    mi, md = pdist.merge_shard_topk(torch.stack(li), torch.stack(ld_), [b[0] for b in bounds])
+    torch.cuda.synchronize()
+    assert np.array_equal(res[0][0], mi.cpu().numpy())
+    assert np.array_equal(res[0][1].view(np.uint32), md.cpu().numpy().view(np.uint32))
+    gt, _ = fodg.exact_topk_batch(fodg.Dataset.from_array(data), queries, 10)
+    ids = res[0][0].astype(np.int64)
+    rec = np.mean([len(set(ids[q]) & set(gt[q].astype(np.int64))) / 10 for q in range(nq)])
+    assert rec >= 0.95, rec
