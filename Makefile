@@ -19,7 +19,7 @@ CLI     := $(PKG)/lib/fodg
 
 all: $(LIB) $(if $(HOST_SRC),$(FODG)) $(CLI) oracle refsuite
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/kernels.hpp include/cagra/capi.h
+build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/kernels.hpp $(PKG)/csrc/host_util.hpp include/cagra/capi.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

@@ -474,10 +474,28 @@ def run_query_sharded(args, D):
     data, queries = make_inputs(args, world, rank)
     ds = fodg.Dataset.from_array(data)
     want_knn = rank == 0 and world == 1 and not args.no_cpu and not args.no_opt_parity
-    r, first_build, build_wall = build_graph(args, ds, local, want_knn)
-    g, binfo = r[0], r[1]
-    knn = r[2] if want_knn else None
-    kstats = knn_stats(args, args.n, binfo)
+    if world > 1:
+        # row-sharded build: each rank computes N/world kNN rows, one
+        # all-gather, every rank optimizes (bit-identical to a 1-GPU build)
+        from paper_2308_15136_b200 import dist as pdist
+
+        D.barrier()
+        t0 = time.perf_counter()
+        g, rinfo = pdist.build_graph_row_sharded(ds, args.degree, local)
+        D.barrier()
+        build_wall = time.perf_counter() - t0
+        (build_wall,) = D.max([build_wall])
+        binfo = {"knn_seconds": rinfo["knn_rows_seconds"] + rinfo["gather_seconds"],
+                 "optimize_seconds": rinfo["optimize_seconds"]}
+        first_build = {"row_sharded": rinfo}
+        knn = None
+        kstats = {"path": "row-sharded over ranks: cagra_exact_knn_rows + all-gather + optimize",
+                  "rows_per_rank": rinfo["rows"]}
+    else:
+        r, first_build, build_wall = build_graph(args, ds, local, want_knn)
+        g, binfo = r[0], r[1]
+        knn = r[2] if want_knn else None
+        kstats = knn_stats(args, args.n, binfo)
     gt, _ = fodg.exact_topk_batch(ds, queries, 10, device=local)
     ix = fodg.Index(ds, g, device=local)
     prm = search_params(args)

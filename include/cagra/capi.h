@@ -134,6 +134,14 @@ uint64_t cagra_mix_seed(uint64_t x);
 int cagra_exact_knn_graph(const float* data, uint32_t n, uint32_t dim, uint32_t k,
                           int device, uint32_t* ids_out, float* dists_out);
 
+/* Rows [row_begin, row_end) of exact_knn_graph(data, k) (knn_build.cpp:40-63:
+ * the parallel_for over rows at :49, one contiguous range) — bit-identical to
+ * those rows of the full graph.  Outputs (row_end - row_begin) x k.  The unit
+ * of a row-sharded multi-GPU / multi-process kNN build. */
+int cagra_exact_knn_rows(const float* data, uint32_t n, uint32_t dim, uint32_t k,
+                         uint32_t row_begin, uint32_t row_end, int device, uint32_t* ids_out,
+                         float* dists_out);
+
 /* exact_topk (topk.hpp:20) for a batch of queries: k nearest by (dist, id). */
 int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* queries,
                      uint32_t nq, uint32_t k, int device, uint32_t* ids_out,
@@ -243,6 +251,47 @@ int cagra_search_dev(cagra_index* index, const float* d_queries, uint32_t nq,
 
 /* Number of kernels the last search call on this index launched. */
 uint32_t cagra_last_launch_count(const cagra_index* index);
+
+/* ---- multi-GPU in one process ---------------------------- */
+/* The reference has no distributed code: batch_search is a parallel_for over
+ * queries (engine.cpp:95-120) and exact_knn_graph one over rows
+ * (knn_build.cpp:49).  These spread the same work over a device set; results
+ * equal the one-device calls (replicated search and the row-sharded build
+ * bit for bit).  `devices` may repeat a device. */
+enum { CAGRA_SHARD_REPLICATE = 0, CAGRA_SHARD_DATASET = 1 };
+
+/* cagra_build_graph with the exact kNN rows computed on every device of the
+ * set (contiguous row ranges, peer-copied to devices[0], optimize there). */
+int cagra_build_graph_multi(const float* data, uint32_t n, uint32_t dim, uint32_t d_init,
+                            uint32_t d, const int* devices, uint32_t ndev, uint32_t* graph_out,
+                            uint32_t* knn_ids_out, float* knn_dists_out, double* seconds_out);
+
+/* exact_knn_graph (knn_build.hpp:40) with the rows spread over the device set. */
+int cagra_exact_knn_graph_multi(const float* data, uint32_t n, uint32_t dim, uint32_t k,
+                                const int* devices, uint32_t ndev, uint32_t* ids_out,
+                                float* dists_out);
+
+typedef struct cagra_mindex cagra_mindex;
+/* CAGRA_SHARD_REPLICATE: a replica of (data, graph) per device; graph NULL =
+ * built with cagra_build_graph_multi (d_init = 2 degree).
+ * CAGRA_SHARD_DATASET: device g holds ids [g n/G, (g+1) n/G) with its own
+ * graph of `degree` built there (graph must be NULL). */
+int cagra_mindex_create(const float* data, uint32_t n, uint32_t dim, const uint32_t* graph,
+                        uint32_t degree, const int* devices, uint32_t ndev, uint32_t shard_mode,
+                        cagra_mindex** out);
+int cagra_mindex_destroy(cagra_mindex* index);
+int cagra_mindex_info(const cagra_mindex* index, uint32_t* n, uint32_t* dim, uint32_t* degree,
+                      uint32_t* parts, uint32_t* shard_mode);
+/* batch_search over the set (host buffers, synchronous).  Replicated: the
+ * batch is split into contiguous slices, one per device, each query keeping
+ * its global seed.  Dataset-sharded: every device searches every query, the
+ * per-shard top-k lists are stored into devices[0]'s gather buffer (peer
+ * stores over NVLink) and merged by K8; stats sum evaluations / resets over
+ * the shards, iterations are the maximum. */
+int cagra_msearch(cagra_mindex* index, const float* queries, uint32_t nq, uint32_t dim,
+                  const cagra_search_params* params, const cagra_engine_opts* opts,
+                  uint32_t* ids_out, float* dists_out, uint32_t* counts_out,
+                  cagra_search_stats* stats_out);
 
 /* ---- dataset-sharded merge (K8) ------------------------------------------ */
 /* Merge G per-shard top-k lists into one top-k per query by (dist, id).

@@ -89,6 +89,8 @@ EXPORTS = [
     "cagra_index_destroy", "cagra_index_info", "cagra_index_row_stride", "cagra_search",
     "cagra_search_dev", "cagra_last_launch_count", "cagra_merge_shard_topk_dev",
     "cagra_graph_metrics", "cagra_trim_scratch", "cagra_knn_last_filter",
+    "cagra_exact_knn_rows", "cagra_build_graph_multi", "cagra_mindex_create",
+    "cagra_mindex_destroy", "cagra_mindex_info", "cagra_msearch", "cagra_exact_knn_graph_multi",
 ]
 
 _lib = None
@@ -132,6 +134,15 @@ def lib() -> C.CDLL:
         L.cagra_last_launch_count.restype = u32
         L.cagra_last_launch_count.argtypes = [vp]
         L.cagra_merge_shard_topk_dev.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, i32, vp]
+        L.cagra_exact_knn_rows.argtypes = [vp, u32, u32, u32, u32, u32, i32, vp, vp]
+        L.cagra_build_graph_multi.argtypes = [vp, u32, u32, u32, u32, vp, u32, vp, vp, vp, vp]
+        L.cagra_mindex_create.argtypes = [vp, u32, u32, vp, u32, vp, u32, u32, C.POINTER(vp)]
+        L.cagra_mindex_destroy.argtypes = [vp]
+        L.cagra_mindex_info.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.cagra_msearch.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp, vp, vp]
+        L.cagra_exact_knn_graph_multi.argtypes = [vp, u32, u32, u32, vp, u32, vp, vp]
+        L.cagra_trim_scratch.argtypes = [i32]
+        L.cagra_knn_last_filter.argtypes = [vp, vp]
         _lib = L
     return _lib
 

@@ -15,135 +15,17 @@
 
 #include "cagra/capi.h"
 #include "common.cuh"
+#include "host_util.hpp"
 #include "kernels.hpp"
 
 namespace cagra {
-namespace {
 
-thread_local std::string g_err;
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return CAGRA_OK;
-  } catch (const UsageErr& e) {
-    g_err = e.what();
-    return CAGRA_ERR_USAGE;
-  } catch (const FormatErr& e) {
-    g_err = e.what();
-    return CAGRA_ERR_FORMAT;
-  } catch (const LogicErr& e) {
-    g_err = e.what();
-    return CAGRA_ERR_LOGIC;
-  } catch (const CudaErr& e) {
-    g_err = e.what();
-    return CAGRA_ERR_CUDA;
-  } catch (const std::bad_alloc&) {
-    g_err = "host allocation failed";
-    return CAGRA_ERR_CUDA;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return CAGRA_ERR_LOGIC;
-  }
-}
-
-int resolve_device(int device) {
-  int count = 0;
-  cudaError_t e = cudaGetDeviceCount(&count);
-  if (e != cudaSuccess || count == 0)
-    throw CudaErr("no CUDA device available (the B200 engine has no CPU path)");
-  int dev = device < 0 ? 0 : device;
-  if (dev >= count) throw UsageErr("device index out of range");
-  return dev;
-}
-
-struct DeviceScope {
-  int prev = -1;
-  explicit DeviceScope(int dev) {
-    cudaGetDevice(&prev);
-    CAGRA_CUDA_TRY(cudaSetDevice(dev));
-  }
-  ~DeviceScope() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-// Owning device allocation.
-struct DBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  DBuf() = default;
-  explicit DBuf(size_t b) { alloc(b); }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { release(); }
-  void alloc(size_t b) {
-    release();
-    if (b == 0) b = 16;
-    CAGRA_CUDA_TRY(cudaMalloc(&p, b));
-    bytes = b;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <class T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-};
-
-struct Stream {
-  cudaStream_t s = nullptr;
-  Stream() { CAGRA_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
-  ~Stream() {
-    if (s) cudaStreamDestroy(s);
-  }
-  void sync() { CAGRA_CUDA_TRY(cudaStreamSynchronize(s)); }
-};
-
-struct Event {
-  cudaEvent_t e = nullptr;
-  Event() { CAGRA_CUDA_TRY(cudaEventCreate(&e)); }
-  ~Event() {
-    if (e) cudaEventDestroy(e);
-  }
-};
-
-int sm_count_of(int dev) {
-  int sms = 0;
-  CAGRA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  return sms;
-}
-
-uint32_t row_stride(uint32_t dim) { return round_up_u32(dim, 4); }
-
-// rows of `dim` floats -> device rows of `ld` floats (zero padded)
-void upload_rows(float* dst, const float* src, uint64_t rows, uint32_t dim, uint32_t ld,
-                 cudaStream_t s, bool src_is_device = false) {
-  if (rows == 0) return;
-  cudaMemcpyKind kind = src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  if (ld == dim) {
-    CAGRA_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(float) * rows * dim, kind, s));
-  } else {
-    CAGRA_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(float) * rows * ld, s));
-    CAGRA_CUDA_TRY(cudaMemcpy2DAsync(dst, sizeof(float) * ld, src, sizeof(float) * dim,
-                                     sizeof(float) * dim, rows, kind, s));
-  }
-}
-
-void read_flag(int* d_flag, int* h, cudaStream_t s) {
-  CAGRA_CUDA_TRY(cudaMemcpyAsync(h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CAGRA_CUDA_TRY(cudaStreamSynchronize(s));
+std::string& last_error_slot() {
+  thread_local std::string err;
+  return err;
 }
 
 // ---- optimize pipeline on device (graph_opt.cpp:211-246) ----
-struct OptOut {
-  float ms[5] = {0, 0, 0, 0, 0};
-};
-
 void optimize_device(const uint32_t* d_knn, const float* d_dists, uint32_t n, uint32_t deg,
                      uint32_t d, bool reorder, bool add_reverse, uint32_t* d_out,
                      cudaStream_t s, OptOut* times) {
@@ -199,7 +81,6 @@ void optimize_device(const uint32_t* d_knn, const float* d_dists, uint32_t n, ui
   }
 }
 
-}  // namespace
 }  // namespace cagra
 
 using namespace cagra;
@@ -389,7 +270,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
 
 extern "C" {
 
-const char* cagra_last_error(void) { return g_err.c_str(); }
+const char* cagra_last_error(void) { return last_error_slot().c_str(); }
 
 const char* cagra_version(void) { return "cagra-b200 0.1 (sm_100a)"; }
 
@@ -453,6 +334,32 @@ int cagra_exact_knn_graph(const float* data, uint32_t n, uint32_t dim, uint32_t 
     CAGRA_CUDA_TRY(cudaMemcpyAsync(ids_out, di.p, sizeof(uint32_t) * (size_t)n * k,
                                    cudaMemcpyDeviceToHost, st.s));
     CAGRA_CUDA_TRY(cudaMemcpyAsync(dists_out, ds.p, sizeof(float) * (size_t)n * k,
+                                   cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+  });
+}
+
+int cagra_exact_knn_rows(const float* data, uint32_t n, uint32_t dim, uint32_t k,
+                         uint32_t row_begin, uint32_t row_end, int device, uint32_t* ids_out,
+                         float* dists_out) {
+  return guarded([&] {
+    if (k == 0 || k >= n) throw UsageErr("exact_knn_graph: require 1 <= k < N");
+    if (dim == 0) throw UsageErr("dataset dimension must be >= 1");
+    if (row_begin > row_end || row_end > n) throw UsageErr("kNN rows: range outside [0, N]");
+    const uint32_t cnt = row_end - row_begin;
+    if (cnt == 0) return;
+    int dev = resolve_device(device);
+    DeviceScope scope(dev);
+    Stream st;
+    uint32_t ld = row_stride(dim);
+    DBuf dd(sizeof(float) * (size_t)n * ld), di(sizeof(uint32_t) * (size_t)cnt * k),
+        ds(sizeof(float) * (size_t)cnt * k);
+    upload_rows(dd.as<float>(), data, n, dim, ld, st.s);
+    launch_exact_topk(dd.as<float>(), n, ld, dd.as<float>() + (size_t)row_begin * ld, cnt, ld,
+                      dim, k, true, di.as<uint32_t>(), ds.as<float>(), st.s, row_begin);
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(ids_out, di.p, sizeof(uint32_t) * (size_t)cnt * k,
+                                   cudaMemcpyDeviceToHost, st.s));
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(dists_out, ds.p, sizeof(float) * (size_t)cnt * k,
                                    cudaMemcpyDeviceToHost, st.s));
     st.sync();
   });

@@ -1114,15 +1114,16 @@ struct Dev {
 // Grow-only per-device scratch of the main kNN path (operand rows, norms,
 // candidate buffers).  A cold 4 GB cudaMalloc costs tens to hundreds of ms of
 // host time inside the build; repeated builds (shards, ground truth, benches)
-// reuse the same memory.  cagra_trim_scratch() releases it.  Builds in one
-// process are serialised by g_knn_mu (they share the arena).
+// reuse the same memory.  cagra_trim_scratch() releases it.  Builds on one
+// device are serialised by that device's g_knn_mu (they share its arena);
+// builds on different devices run concurrently (row-sharded multi-GPU build).
 enum ArenaSlot { kSlotP, kSlotR, kSlotQn, kSlotXn, kSlotMax, kSlotMu, kSlotPart, kSlotLists,
                  kSlotBufs, kSlotBcount, kSlotFails, kSlotRer, kSlotCount };
 struct Arena {
   void* p[kSlotCount] = {};
   size_t cap[kSlotCount] = {};
 };
-std::mutex g_knn_mu;
+std::mutex g_knn_mu[64];
 Arena g_arena[64];
 struct View {  // non-owning view of an arena slot
   void* p;
@@ -1217,9 +1218,9 @@ uint32_t tc_halves(uint32_t kblocks, uint32_t pend_cap) {
 KnnTcStats g_knn_tc_stats;
 
 void knn_trim_scratch(int device) {
-  std::lock_guard<std::mutex> lk(g_knn_mu);
   for (int d = 0; d < 64; ++d) {
     if (device >= 0 && d != device) continue;
+    std::lock_guard<std::mutex> lk(g_knn_mu[d]);
     Arena& a = g_arena[d];
     for (int i = 0; i < kSlotCount; ++i) {
       if (!a.p[i]) continue;
@@ -1477,7 +1478,9 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
                    uint32_t nq, uint32_t qld, uint32_t dim, uint32_t K, bool exclude_self,
                    uint32_t self_base, uint32_t* d_ids, float* d_dists, cudaStream_t stream) {
   if (nq == 0) return;
-  std::lock_guard<std::mutex> lk(g_knn_mu);
+  int lk_dev = 0;
+  CAGRA_CUDA_TRY(cudaGetDevice(&lk_dev));
+  std::lock_guard<std::mutex> lk(g_knn_mu[lk_dev & 63]);
   Tracer tr(stream);
   tr.mark("start");
   TcCall c;

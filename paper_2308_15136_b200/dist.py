@@ -73,6 +73,50 @@ def merge_shard_topk(stacked_ids, stacked_dists, offsets, device: int = 0, strea
     return out_i, out_d
 
 
+def build_graph_row_sharded(ds: fodg.Dataset, degree: int, device: int = 0, group=None,
+                            d_init: Optional[int] = None):
+    """Row-sharded multi-process graph build: rank r
+    computes the exact kNN rows of its contiguous row range on its GPU
+    (cagra_exact_knn_rows — the parallel_for over rows of knn_build.cpp:49,
+    split over ranks), ONE all-gather assembles the N x d_init kNN graph on
+    every rank, and each rank runs the rank optimize (graph_opt.cpp:211-246)
+    locally, so no second collective is needed.  The graph is bit-identical
+    to a one-GPU build.  Returns (Graph, info)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    d_init = d_init or 2 * degree
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = ds.size()
+    bounds = shard_bounds(n, world)
+    s, e = bounds[rank]
+    t0 = time.perf_counter()
+    part = fodg.exact_knn_rows(ds, d_init, s, e, device)
+    t_rows = time.perf_counter() - t0
+    maxr = max(b - a for a, b in bounds)
+    nccl = dist.get_backend(group) == "nccl"
+    where = torch.device("cuda", device) if nccl else torch.device("cpu")
+    ids = torch.zeros((maxr, d_init), dtype=torch.int32, device=where)
+    dists = torch.zeros((maxr, d_init), dtype=torch.float32, device=where)
+    ids[:e - s] = torch.from_numpy(part.ids.view(np.int32)).to(where)
+    dists[:e - s] = torch.from_numpy(part.dists).to(where)
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    gd = [torch.empty_like(dists) for _ in range(world)]
+    dist.all_gather(gi, ids, group=group)
+    dist.all_gather(gd, dists, group=group)
+    kid = np.concatenate([gi[r][:b - a].cpu().numpy().view(np.uint32)
+                          for r, (a, b) in enumerate(bounds)])
+    kd = np.concatenate([gd[r][:b - a].cpu().numpy() for r, (a, b) in enumerate(bounds)])
+    t_gather = time.perf_counter() - t0 - t_rows
+    st = fodg.OptimizeStats()
+    g = fodg.optimize(fodg.KnnGraph(n, d_init, kid, kd), degree,
+                      fodg.OptimizeOptions(device=device), stats=st)
+    return g, {"knn_rows_seconds": t_rows, "gather_seconds": t_gather,
+               "optimize_seconds": st.total_seconds, "rows": e - s}
+
+
 class ShardedIndex:
     """This rank's shard of a dataset-sharded index (ids local to the shard).
 

@@ -460,6 +460,101 @@ def build_graph(ds: Dataset, d: int, d_init: Optional[int] = None, device: int =
     return g, info
 
 
+def exact_knn_rows(ds: Dataset, k: int, row_begin: int, row_end: int,
+                   device: int = 0) -> KnnGraph:
+    """Rows [row_begin, row_end) of exact_knn_graph(ds, k) (knn_build.cpp:40-63,
+    the parallel_for over rows at :49, one range): the unit of a row-sharded
+    build.  Returns a KnnGraph of row_end - row_begin rows (global ids)."""
+    n, dim = ds.data.shape
+    cnt = row_end - row_begin
+    ids = np.empty((cnt, k), np.uint32)
+    dists = np.empty((cnt, k), np.float32)
+    check(lib().cagra_exact_knn_rows(ptr(ds.data), n, dim, k, row_begin, row_end, device,
+                                     ptr(ids), ptr(dists)))
+    return KnnGraph(cnt, k, ids, dists)
+
+
+def _devset(devices: Sequence[int]):
+    arr = np.ascontiguousarray(np.asarray(list(devices), np.int32))
+    if arr.size == 0:
+        raise UsageError("device set: empty")
+    return arr
+
+
+def build_graph_multi(ds: Dataset, d: int, devices: Sequence[int], d_init: Optional[int] = None,
+                      return_knn: bool = False):
+    """build_graph with the exact kNN rows spread over `devices` (row-sharded
+    K1, peer copies to devices[0], optimize there) — bit-identical graph."""
+    d_init = d_init or 2 * d
+    n, dim = ds.data.shape
+    dv = _devset(devices)
+    out = np.empty((n, d), np.uint32)
+    kid = np.empty((n, d_init), np.uint32) if return_knn else None
+    kd = np.empty((n, d_init), np.float32) if return_knn else None
+    secs = np.zeros(2, np.float64)
+    check(lib().cagra_build_graph_multi(ptr(ds.data), n, dim, d_init, d, ptr(dv), dv.size,
+                                        ptr(out), ptr(kid), ptr(kd), ptr(secs)))
+    g = Graph(n, d, out)
+    info = {"knn_seconds": float(secs[0]), "optimize_seconds": float(secs[1])}
+    if return_knn:
+        return g, info, KnnGraph(n, d_init, kid, kd)
+    return g, info
+
+
+class MultiIndex:
+    """A device set in one process (cagra_mindex): `replicate` = a replica
+    per device with the batch split over them (same results as one device);
+    `dataset` = contiguous id-range shards with their own graphs, every query
+    searched on every shard, per-shard top-k merged by K8 on devices[0]."""
+
+    MODES = {"replicate": 0, "dataset": 1}
+
+    def __init__(self, ds, devices: Sequence[int], graph=None, degree: int = 64,
+                 shard_mode: str = "replicate"):
+        data = ds.data if isinstance(ds, Dataset) else np.ascontiguousarray(ds, np.float32)
+        self._data = data
+        gids = None
+        if graph is not None:
+            gids = graph.ids if isinstance(graph, Graph) else np.asarray(graph)
+            gids = np.ascontiguousarray(gids.reshape(data.shape[0], -1), np.uint32)
+            degree = gids.shape[1]
+        self._graph = gids
+        dv = _devset(devices)
+        h = C.c_void_p()
+        check(lib().cagra_mindex_create(ptr(data), data.shape[0], data.shape[1], ptr(gids),
+                                        degree, ptr(dv), dv.size, self.MODES[shard_mode],
+                                        C.byref(h)))
+        self.h = h
+        self.dim = data.shape[1]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cagra_mindex_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, queries, params: SearchParams, options: Optional[EngineOptions] = None,
+               query_offset: int = 0):
+        """(ids [nq,k], dists [nq,k], counts [nq], stats recarray)."""
+        options = options or EngineOptions()
+        qs = _as_rows(queries)
+        nq, k = qs.shape[0], params.k
+        ids = np.empty((nq, k), np.uint32)
+        dists = np.empty((nq, k), np.float32)
+        counts = np.empty(nq, np.uint32)
+        stats = np.empty(nq, capi.STATS_DTYPE)
+        pc, oc = params.c(), options.c(0, query_offset)
+        check(lib().cagra_msearch(self.h, ptr(qs), nq, qs.shape[1] if nq else self.dim,
+                                  C.byref(pc), C.byref(oc), ptr(ids), ptr(dists), ptr(counts),
+                                  ptr(stats)))
+        return ids, dists, counts, stats
+
+
 # ------------------------------------------------------------------- search --
 @dataclass
 class GraphQualityReport:

@@ -129,8 +129,15 @@ struct CacheEntry {
     const void* ids;
     std::uint32_t n, dim, degree;
     std::uint64_t h_data, h_ids;
-    cagra_index* ix;
+    cagra_index* ix;     // single device, or
+    cagra_mindex* mx;    // the CAGRA_DEVICES set
+    std::vector<int> devs;
 };
+
+void destroy(CacheEntry& e) {
+    if (e.ix) cagra_index_destroy(e.ix);
+    if (e.mx) cagra_mindex_destroy(e.mx);
+}
 
 std::mutex g_mu;
 std::list<CacheEntry> g_cache;  // most recent first
@@ -138,33 +145,54 @@ constexpr std::size_t kMaxCached = 4;
 
 }  // namespace
 
-cagra_index* index_for(const Graph& graph, const Dataset& ds) {
+namespace {
+
+// Looks up (or uploads) the device copy of (graph, ds) for `devs`: one
+// device -> cagra_index, several -> a replicated cagra_mindex.
+CacheEntry& entry_for(const Graph& graph, const Dataset& ds, const std::vector<int>& devs) {
     const bool identity = trust_identity();
     const std::uint64_t hd = identity ? 0 : content_hash(ds.raw(), 4ull * ds.size() * ds.dim());
     const std::uint64_t hi = identity ? 0 : content_hash(graph.ids.data(), 4ull * graph.ids.size());
-    std::lock_guard<std::mutex> lock(g_mu);
     for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
         if (it->data == ds.raw() && it->ids == graph.ids.data() && it->n == ds.size() &&
-            it->dim == ds.dim() && it->degree == graph.degree &&
+            it->dim == ds.dim() && it->degree == graph.degree && it->devs == devs &&
             (identity || (it->h_data == hd && it->h_ids == hi))) {
             g_cache.splice(g_cache.begin(), g_cache, it);
-            return it->ix;
+            return g_cache.front();
         }
     }
-    cagra_index* ix = nullptr;
-    check(cagra_index_create(ds.raw(), ds.size(), ds.dim(), graph.ids.data(), graph.degree,
-                             device(), &ix));
-    g_cache.push_front({ds.raw(), graph.ids.data(), ds.size(), ds.dim(), graph.degree, hd, hi, ix});
+    CacheEntry e{ds.raw(), graph.ids.data(), ds.size(), ds.dim(), graph.degree, hd, hi,
+                 nullptr, nullptr, devs};
+    if (devs.size() == 1)
+        check(cagra_index_create(ds.raw(), ds.size(), ds.dim(), graph.ids.data(), graph.degree,
+                                 devs[0], &e.ix));
+    else
+        check(cagra_mindex_create(ds.raw(), ds.size(), ds.dim(), graph.ids.data(), graph.degree,
+                                  devs.data(), static_cast<std::uint32_t>(devs.size()),
+                                  CAGRA_SHARD_REPLICATE, &e.mx));
+    g_cache.push_front(e);
     while (g_cache.size() > kMaxCached) {
-        cagra_index_destroy(g_cache.back().ix);
+        destroy(g_cache.back());
         g_cache.pop_back();
     }
-    return ix;
+    return g_cache.front();
+}
+
+}  // namespace
+
+cagra_index* index_for(const Graph& graph, const Dataset& ds) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return entry_for(graph, ds, {device()}).ix;
+}
+
+cagra_mindex* mindex_for(const Graph& graph, const Dataset& ds) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return entry_for(graph, ds, devices()).mx;
 }
 
 void invalidate_index_cache() {
     std::lock_guard<std::mutex> lock(g_mu);
-    for (auto& e : g_cache) cagra_index_destroy(e.ix);
+    for (auto& e : g_cache) destroy(e);
     g_cache.clear();
 }
 

@@ -35,6 +35,10 @@ bool fast_distances();
 /// the host buffers are unchanged.
 cagra_index* index_for(const Graph& graph, const Dataset& ds);
 
+/// The replicated device-set index (CAGRA_DEVICES with more than one entry)
+/// for (graph, ds), cached under the same rule as index_for.
+cagra_mindex* mindex_for(const Graph& graph, const Dataset& ds);
+
 /// SM count of device() (the default b_T of choose_mode).
 unsigned device_sm_count();
 

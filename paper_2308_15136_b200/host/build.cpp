@@ -17,8 +17,14 @@ KnnGraph exact_knn_graph(const Dataset& ds, std::uint32_t k, unsigned /*num_thre
     g.degree = k;
     g.ids.resize(static_cast<std::size_t>(g.num_nodes) * k);
     g.dists.resize(g.ids.size());
-    b200::check(cagra_exact_knn_graph(ds.raw(), ds.size(), ds.dim(), k, b200::device(),
-                                      g.ids.data(), g.dists.data()));
+    const std::vector<int> devs = b200::devices();
+    if (devs.size() > 1)  // CAGRA_DEVICES: rows spread over the set (row-sharded K1)
+        b200::check(cagra_exact_knn_graph_multi(ds.raw(), ds.size(), ds.dim(), k, devs.data(),
+                                                static_cast<std::uint32_t>(devs.size()),
+                                                g.ids.data(), g.dists.data()));
+    else
+        b200::check(cagra_exact_knn_graph(ds.raw(), ds.size(), ds.dim(), k, devs[0],
+                                          g.ids.data(), g.dists.data()));
     return g;
 }
 

@@ -26,9 +26,9 @@ def _bin(name):
     return path
 
 
-def _run(path, *args, timeout=1200):
+def _run(path, *args, timeout=1200, env=None):
     return subprocess.run([path, *args], capture_output=True, text=True, timeout=timeout,
-                          cwd="/tmp")
+                          cwd="/tmp", env=env)
 
 
 @pytest.mark.parametrize("suite", HOST_ONLY)
@@ -46,6 +46,19 @@ def test_reference_unit_suite_on_b200(gpu, suite):
     assert r.returncode == 0, summary[0] + "\n" + r.stderr[-4000:]
     m = re.search(r"(\d+) failed \| checks: (\d+) \| (\d+) failed", summary[0])
     assert m and int(m.group(1)) == 0 and int(m.group(3)) == 0, summary[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["test_knn_build", "test_engine", "test_search"])
+def test_reference_suite_over_device_set(gpu, suite):
+    # the drop-in with CAGRA_DEVICES=0,0: exact_knn_graph row-sharded over the
+    # set and batch_search split over replicas (cagra_mindex) — the reference's
+    # own checks (thread-count independence, bit-equal distances, batch ==
+    # search_one) hold unchanged
+    env = dict(os.environ, CAGRA_DEVICES="0,0")
+    r = _run(_bin(suite), env=env)
+    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest-compat]")]
+    assert summary and r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 @pytest.mark.gpu
