@@ -105,7 +105,9 @@ struct cagra_index {
   SearchConfig plan_cfg{};
   uint32_t plan_nq = 0;
   bool plan_valid = false;
-  bool mc_layout = false;     // tables currently laid out per query
+  int mc_layout = 0;          // tables laid out: 0 per CTA, 1 per query (generic
+                              // multi-CTA), 2 per query x 2 regions (batch-1 kernel)
+  DBuf b1_ctr;                // batch-1 kernel: teams finished per query (zeroed)
   // Completion of the last search issued on this index, on whatever stream
   // it ran.  Every search first makes its stream wait on it and records it
   // again at the end, so calls on different streams (cagra_search on the
@@ -120,6 +122,18 @@ struct cagra_index {
 };
 
 namespace {
+
+// A host pointer the device can dereference directly (pinned memory mapped
+// into the unified address space: the same address on both sides).
+bool host_mapped(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
 
 // Grows a per-index scratch buffer after the index's previous search is done.
 void grow(cagra_index* ix, DBuf& b, size_t bytes) {
@@ -224,7 +238,8 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
     grow(ix, ix->team_out, sizeof(unsigned long long) * std::max<size_t>(pl.team_elems, 1));
     grow(ix, ix->team_stats, sizeof(cagra_search_stats) * (size_t)nq * pl.teams);
     // per-query regions tagged by a call generation; a new layout starts clean
-    if (!ix->mc_layout || pl.hcap != ix->table_hcap || pl.table_elems > ix->table_elems ||
+    const int kind = pl.b1 ? 2 : 1;
+    if (ix->mc_layout != kind || pl.hcap != ix->table_hcap || pl.table_elems > ix->table_elems ||
         ix->mc_tag == 0xffffffffu) {
       if (pl.table_elems > ix->table_elems) {
         grow(ix, ix->tables, sizeof(unsigned long long) * pl.table_elems);
@@ -236,12 +251,16 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
       ix->table_grid = 0;  // the per-CTA generations no longer match
       grow(ix, ix->gens, sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
-      ix->mc_layout = true;
+      ix->mc_layout = kind;
+    }
+    if (pl.b1 && ix->b1_ctr.bytes < sizeof(uint32_t) * nq) {
+      grow(ix, ix->b1_ctr, sizeof(uint32_t) * nq);
+      CAGRA_CUDA_TRY(cudaMemsetAsync(ix->b1_ctr.p, 0, ix->b1_ctr.bytes, s));
     }
     ix->mc_tag++;
     grow(ix, ix->gens, sizeof(uint32_t) * pl.grid);
   } else if (pl.table_elems) {
-    bool relayout = ix->mc_layout || pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
+    bool relayout = ix->mc_layout != 0 || pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
                     pl.table_elems > ix->table_elems;
     if (relayout) {
       // a changed layout would alias old tags into other slots: start clean
@@ -254,7 +273,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
       ix->table_hcap = pl.hcap;
       ix->table_grid = std::max(pl.grid, ix->table_grid);
-      ix->mc_layout = false;
+      ix->mc_layout = 0;
     }
   } else {
     grow(ix, ix->gens, sizeof(uint32_t) * pl.grid);
@@ -263,7 +282,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
                                     ix->init_ids.as<uint32_t>(), ix->work.as<uint32_t>(),
                                     ix->tables.as<unsigned long long>(), ix->gens.as<uint32_t>(),
                                     ix->team_out.as<unsigned long long>(), ix->team_stats.p,
-                                    ix->mc_tag, s);
+                                    ix->mc_tag, s, ix->b1_ctr.as<uint32_t>());
 }
 
 }  // namespace
@@ -725,6 +744,23 @@ int cagra_search(cagra_index* ix, const float* queries, uint32_t nq, uint32_t di
     cudaStream_t s = ix->stream->s;
     const uint32_t k = params->k;
     begin_on(ix, s);
+    // Small batches whose host buffers are device-accessible (pinned,
+    // cudaHostAlloc'd: mapped under UVA) skip the staging copies: the kernels
+    // read the query rows once per CTA and write the k results once, straight
+    // over PCIe/C2C (the batch-1 latency path: one launch, no memcpy).
+    if (nq <= 64 && dim == ix->ld && host_mapped(queries) && host_mapped(ids_out) &&
+        host_mapped(dists_out) && (!counts_out || host_mapped(counts_out)) &&
+        (!stats_out || host_mapped(stats_out))) {
+      uint32_t* counts = counts_out;
+      if (!counts) {
+        grow(ix, ix->counts, sizeof(uint32_t) * nq);
+        counts = ix->counts.as<uint32_t>();
+      }
+      run_search(ix, queries, nq, params, o, ids_out, dists_out, counts, stats_out, s);
+      end_on(ix, s);
+      CAGRA_CUDA_TRY(cudaStreamSynchronize(s));
+      return;
+    }
     grow(ix, ix->q, sizeof(float) * (size_t)nq * ix->ld);
     grow(ix, ix->ids, sizeof(uint32_t) * (size_t)nq * k);
     grow(ix, ix->dists, sizeof(float) * (size_t)nq * k);

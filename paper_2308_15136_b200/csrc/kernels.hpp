@@ -109,6 +109,7 @@ struct SearchPlan {
   size_t table_elems = 0;  // u64 slots of HBM visited tables (grid * hcap)
   size_t init_elems = 0;   // u32 init sample ids
   bool mc = false;         // shared mode with one CTA per (query, team)
+  bool b1 = false;         // mc via the fused small-team kernel (search_b1.cu)
   size_t team_elems = 0;   // u64 team top-M keys (nq * teams * M) in mc mode
   const void* fn = nullptr;
 };
@@ -124,7 +125,18 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
                        uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
                        uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
                        unsigned long long* d_team_out, void* d_team_stats, uint32_t mc_tag,
-                       cudaStream_t stream);
+                       cudaStream_t stream, uint32_t* d_b1_ctr = nullptr);
+
+// ---- search_b1.cu: multi-CTA shared mode, one 128-thread CTA per team ------
+// with the team merge in the query's last CTA (one launch per batch)
+bool team_b1_eligible(uint32_t M, uint32_t k, uint32_t T, uint32_t degree, uint32_t ld);
+void launch_team_b1(const float* data, const uint32_t* graph, uint32_t n, uint32_t ld,
+                    uint32_t dim, uint32_t degree, const float* queries, uint32_t nq, uint32_t T,
+                    uint32_t M, uint32_t k, uint32_t max_iter, uint32_t min_iter, uint64_t seed,
+                    uint64_t query_offset, uint32_t seed_mode, uint32_t* tab, uint32_t hcap,
+                    uint32_t tag, unsigned long long* team_out, void* team_stats,
+                    uint32_t* done_ctr, uint32_t* out_ids, float* out_dists,
+                    uint32_t* out_counts, void* stats, cudaStream_t stream);
 
 // ---- merge.cu (K8) --------------------------------------------------------------
 void launch_shard_merge(const uint32_t* d_shard_ids, const float* d_shard_dists,

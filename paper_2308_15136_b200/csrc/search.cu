@@ -1567,6 +1567,11 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   }
   pl.grid = (uint32_t)grid;
   pl.init_elems = (size_t)nq * T * C;
+  if (pl.mc && team_b1_eligible(c.topm, c.k, T, d, ix.ld)) {
+    const char* e = std::getenv("CAGRA_B1_KERNEL");  // "0": the generic multi-CTA kernel
+    pl.b1 = !(e && e[0] == '0');
+    if (pl.b1) pl.grid = nq * T;
+  }
   return pl;
 }
 
@@ -1575,7 +1580,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
                        uint32_t* d_counts, void* d_stats, uint32_t* d_init_ids,
                        uint32_t* d_work, unsigned long long* d_tables, uint32_t* d_gens,
                        unsigned long long* d_team_out, void* d_team_stats, uint32_t mc_tag,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, uint32_t* d_b1_ctr) {
   if (nq == 0) return 0;
   // small per-item sample counts are generated inside the search kernel (one
   // launch less on the batch-1 path); the lockstep shared kernel and large
@@ -1590,7 +1595,7 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
     CAGRA_LAUNCH_CHECK();
     ++launches;
   }
-  CAGRA_CUDA_TRY(cudaMemsetAsync(d_work, 0, sizeof(uint32_t), stream));
+  if (!pl.b1) CAGRA_CUDA_TRY(cudaMemsetAsync(d_work, 0, sizeof(uint32_t), stream));
   KParams P;
   P.data = ix.data;
   P.graph = ix.graph;
@@ -1614,8 +1619,17 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.mc_teams = pl.mc ? pl.teams : 0;
   P.mc_tag = mc_tag;
   P.mc_tab = pl.mc ? reinterpret_cast<uint32_t*>(d_tables) : nullptr;
-  if (pl.mc)  // one visited region per query, emptied for this call (one CAS per insert)
+  if (pl.mc && !pl.b1)  // one visited region per query, emptied for this call
     CAGRA_CUDA_TRY(cudaMemsetAsync(d_tables, 0xff, sizeof(uint32_t) * (size_t)nq * pl.hcap, stream));
+  if (pl.b1) {
+    // one launch: teams + the last team's merge; its two table regions are
+    // cleared alternately inside the kernel
+    launch_team_b1(ix.data, ix.graph, ix.n, ix.ld, ix.dim, ix.degree, d_queries, nq, pl.teams,
+                   c.topm, c.k, pl.max_iter, pl.min_iter, c.seed, c.query_offset, c.seed_mode,
+                   reinterpret_cast<uint32_t*>(d_tables), pl.hcap, mc_tag, d_team_out,
+                   d_team_stats, d_b1_ctr, d_ids, d_dists, d_counts, d_stats, stream);
+    return launches;
+  }
   P.team_out = d_team_out;
   P.team_stats = reinterpret_cast<DevStats*>(d_team_stats);
   P.init_ids = sample_in_kernel ? nullptr : d_init_ids;
