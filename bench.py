@@ -93,8 +93,8 @@ def parse():
                     help="queries in the CPU baseline sample (0 = auto, ~10 s of work)")
     ap.add_argument("--batch1", type=int, default=500,
                     help="also time this many sequential batch-1 calls (0 = off)")
-    ap.add_argument("--b1-topm", type=int, default=16, help="batch-1 team top-M")
-    ap.add_argument("--b1-teams", type=int, default=64, help="batch-1 teams (one CTA each)")
+    ap.add_argument("--b1-topm", type=int, default=10, help="batch-1 team top-M")
+    ap.add_argument("--b1-teams", type=int, default=96, help="batch-1 teams (one CTA each)")
     ap.add_argument("--no-cpu", action="store_true", help="skip every reference (CPU) leg")
     ap.add_argument("--no-opt-parity", action="store_true",
                     help="skip fodg_ref::optimize on the device-built kNN graph")

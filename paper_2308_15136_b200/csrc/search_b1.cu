@@ -140,26 +140,33 @@ __device__ __forceinline__ uint32_t compact_unique(const uint64_t (&v)[E], int l
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+// warp w: the first k entries of teams w, w + 4, ... (32 E keys at most) ->
+// sort -> unique -> first k at dst (dummy padded)
+template <int E>
+__device__ __forceinline__ void b1_merge_quarter(const unsigned long long* lists, uint32_t T,
+                                                 uint32_t M, uint32_t k, int warp, int lane,
+                                                 uint64_t* dst) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = lane * E + e;
+    const uint32_t tl = i / k, j = i - tl * k, team = warp + 4 * tl;
+    v[e] = team < T ? cmp_key(__ldcg(lists + (size_t)team * M + j)) : kDummyKey;
+  }
+  warp_sort_regs<E>(v, lane);
+  const uint32_t tot = compact_unique<E>(v, lane, dst, k);
+  __syncwarp();
+  for (uint32_t i = tot + lane; i < k; i += 32) dst[i] = kDummyKey;
+}
+
 // The query's final top-k from its T team lists (run by its last CTA).
 __device__ void b1_merge(const B1Params& P, uint32_t q, uint64_t* sm) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t T = P.T, M = P.M, k = P.k;
   const unsigned long long* lists = P.team_out + (size_t)q * T * M;
-  // 1) warp w: the first k entries of teams w, w + 4, ... -> 256-key sort ->
-  //    unique -> first k at sm[32 w ...] (dummy padded)
-  {
-    uint64_t v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t i = lane * 8 + e;
-      const uint32_t tl = i / k, j = i - tl * k, team = warp + 4 * tl;
-      v[e] = team < T ? cmp_key(__ldcg(lists + (size_t)team * M + j)) : kDummyKey;
-    }
-    warp_sort_regs<8>(v, lane);
-    const uint32_t tot = compact_unique<8>(v, lane, sm + warp * 32, k);
-    __syncwarp();
-    for (uint32_t i = tot + lane; i < k; i += 32) sm[warp * 32 + i] = kDummyKey;
-  }
+  // 1) per warp: a quarter of the teams' first-k entries
+  if (((T + 3) / 4) * k <= 256) b1_merge_quarter<8>(lists, T, M, k, warp, lane, sm + warp * 32);
+  else b1_merge_quarter<16>(lists, T, M, k, warp, lane, sm + warp * 32);
   __syncthreads();
   if (warp != 0) return;
   // 2) the 4 warps' lists -> sort -> unique -> first k at sm[128 ...]
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
   // its own marks are ordered by that barrier and the init samples are
   // de-duplicated — so survivors never duplicate a top-M entry.)
   uint64_t top = kDummyKey, mth = kDummyKey;
-  uint32_t iter = 0, parent = 0, slot = 0;
+  uint32_t iter = 0, parent = 0, slot = 0, evals = 0;
   bool from_graph = false, finish = false, converged = false;
   for (;;) {
     B1_T(p0);
@@ -348,7 +355,8 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
     if (mine_first) atomicOr(bits + (bi >> 5), 1u << (bi & 31));
     const unsigned fb = __ballot_sync(0xffffffffu, mine_first);
     const uint32_t firstm = (fb >> (lane & ~7)) & 0xfu;
-    // survivors: candidate c's fixed slot holds its key, or a dummy
+    // survivors: candidate c's fixed slot holds its key, or a dummy (the
+    // evaluation count stays in registers until the end)
     uint32_t nev = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -358,9 +366,7 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
         s_surv[slot][warp * 16 + j * 4 + grp] = first && key < mth ? key : kDummyKey;
       nev += (sub == 0 && first) ? 1u : 0u;
     }
-    nev += __shfl_xor_sync(0xffffffffu, nev, 16);
-    nev += __shfl_xor_sync(0xffffffffu, nev, 8);
-    if (lane == 0 && nev) atomicAdd(&s_evals, nev);
+    evals += nev;
     B1_T(p3);
     __syncthreads();
     B1_T(p4);
@@ -432,10 +438,13 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
         parent = __shfl_sync(0xffffffffu, static_cast<uint32_t>(top), pl);
         if (lane == pl) top |= kParentFlag;
         finish = iter >= P.max_iter;  // the expansion below is flushed, then stop
-        // the next unflagged entry is the likely parent after this one: pull
-        // its graph row into L2 while this expansion runs (one warp does it)
-        const unsigned b2 = b & ~(1u << pl);
-        if (warp == 0 && b2 && lane == __ffs(b2) - 1) {
+        // the next two unflagged entries are the likely parents after this
+        // one: pull their graph rows into L2 while this expansion runs
+        unsigned b2 = b & ~(1u << pl);
+        const unsigned b3 = b2 ? b2 & (b2 - 1) : 0u;
+        b2 = b2 & ~b3;  // lowest remaining bit
+        const unsigned pre = b2 | (b3 & (0u - b3));
+        if (warp == 0 && ((pre >> lane) & 1u)) {
           const uint32_t* row = P.graph + (size_t)static_cast<uint32_t>(top) * deg;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
           if (deg * 4 > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 32));
@@ -455,6 +464,10 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
     from_graph = true;
     slot = (slot + 1) % 3;
   }
+  evals += __shfl_xor_sync(0xffffffffu, evals, 16);
+  evals += __shfl_xor_sync(0xffffffffu, evals, 8);
+  if (lane == 0 && evals) atomicAdd(&s_evals, evals);
+  __syncthreads();
   if (warp == 0) {
     if ((uint32_t)lane < P.M) P.team_out[(size_t)item * P.M + lane] = top;
     if (lane == 0) {
@@ -486,9 +499,9 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
 
 bool team_b1_eligible(uint32_t M, uint32_t k, uint32_t T, uint32_t degree, uint32_t ld) {
   // the fused merge: each warp's share of the teams' first-k entries fits one
-  // 256-key warp sort, and the 4 warps' first-k lists one 128-key sort
+  // 512-key warp sort, and the 4 warps' first-k lists one 128-key sort
   const uint32_t share = ((T + 3) / 4) * k;
-  return M >= 1 && M <= 32 && k <= 32 && share <= 256 && degree >= 1 && degree <= 64 &&
+  return M >= 1 && M <= 32 && k <= 32 && share <= 512 && degree >= 1 && degree <= 64 &&
          ld <= 128;
 }
 
