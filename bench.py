@@ -96,6 +96,11 @@ def parse():
     ap.add_argument("--b1-topm", type=int, default=10, help="batch-1 team top-M")
     ap.add_argument("--b1-teams", type=int, default=96, help="batch-1 teams (one CTA each)")
     ap.add_argument("--no-cpu", action="store_true", help="skip every reference (CPU) leg")
+    ap.add_argument("--cpu-topm", type=int, default=CPU_BATCH_POINT["topm"],
+                    help="the reference's own batch operating point (default: its best "
+                         "recall>=0.95 point at 1M x 96)")
+    ap.add_argument("--cpu-width", type=int, default=CPU_BATCH_POINT["width"])
+    ap.add_argument("--cpu-hash", default="standard", choices=["standard", "forgettable"])
     ap.add_argument("--no-opt-parity", action="store_true",
                     help="skip fodg_ref::optimize on the device-built kNN graph")
     ap.add_argument("--build-once", action="store_true",
@@ -671,7 +676,9 @@ def cpu_batch_legs(args, data, graph, queries, gt, gpu_ids):
     parity = id_parity(gpu_ids[:npar], pids, gt[:npar])
     parity["params"] = f"M={args.topm} p={args.width} {args.hash} (the GPU's)"
     # baseline: the reference's own best recall >= 0.95 point
-    pb = ref_params(args, **CPU_BATCH_POINT)
+    pb = ref_params(args, topm=args.cpu_topm, width=args.cpu_width,
+                    hash_policy=1 if args.cpu_hash == "forgettable" else 0,
+                    hash_bits=args.hash_bits if args.cpu_hash == "forgettable" else 11)
     probe = queries[:max(threads, 8)]
     t0 = time.perf_counter()
     rix.batch_search(probe, pb, threads=threads)
@@ -684,8 +691,9 @@ def cpu_batch_legs(args, data, graph, queries, gt, gpu_ids):
     rix.close()
     cpu = {"value": sample / el, "unit": "queries/s", "cores": threads, "kind": "reference",
            **host_cpu(), "recall@10": recall_at_k(ids, gt[:sample]),
-           "operating_point": "per-query M=896 p=16 standard hash: the reference's best "
-                              "recall>=0.95 grid point (profiles/r02_cpu_batch10k_sweep.txt)",
+           "operating_point": f"per-query M={args.cpu_topm} p={args.cpu_width} {args.cpu_hash} "
+                              "hash (default: the reference's best recall>=0.95 grid point at "
+                              "1M x 96, profiles/r02_cpu_batch10k_sweep.txt)",
            "sample": f"first {sample} of the {args.batch} batch queries, same index, "
                      f"fodg::batch_search per-query mode, {threads} threads"}
     return cpu, parity

@@ -106,7 +106,8 @@ struct cagra_index {
   uint32_t plan_nq = 0;
   bool plan_valid = false;
   int mc_layout = 0;          // tables laid out: 0 per CTA, 1 per query (generic
-                              // multi-CTA), 2 per query x 2 regions (batch-1 kernel)
+                              // multi-CTA), 2 per query x 2 regions (batch-1 kernel),
+                              // 3 per-CTA visited bitmaps (standard policy)
   DBuf b1_ctr;                // batch-1 kernel: teams finished per query (zeroed)
   // Completion of the last search issued on this index, on whatever stream
   // it ran.  Every search first makes its stream wait on it and records it
@@ -259,6 +260,14 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
     }
     ix->mc_tag++;
     grow(ix, ix->gens, sizeof(uint32_t) * pl.grid);
+  } else if (pl.bitmap) {
+    // per-CTA bitmaps, cleared by the kernel at every query: no tags to keep
+    if (pl.table_elems > ix->table_elems) {
+      grow(ix, ix->tables, sizeof(unsigned long long) * pl.table_elems);
+      ix->table_elems = pl.table_elems;
+    }
+    grow(ix, ix->gens, sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
+    ix->mc_layout = 3;
   } else if (pl.table_elems) {
     bool relayout = ix->mc_layout != 0 || pl.hcap != ix->table_hcap || pl.grid > ix->table_grid ||
                     pl.table_elems > ix->table_elems;

@@ -110,6 +110,8 @@ struct SearchPlan {
   size_t init_elems = 0;   // u32 init sample ids
   bool mc = false;         // shared mode with one CTA per (query, team)
   bool b1 = false;         // mc via the fused small-team kernel (search_b1.cu)
+  bool bitmap = false;     // standard policy: exact visited bitmap per resident CTA
+  uint32_t bm_words = 0;   // u32 words per CTA bitmap
   size_t team_elems = 0;   // u64 team top-M keys (nq * teams * M) in mc mode
   const void* fn = nullptr;
 };

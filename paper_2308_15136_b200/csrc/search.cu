@@ -70,6 +70,11 @@ struct KParams {
   uint64_t seed, query_offset;
   uint32_t seed_mode;
   unsigned long long* gtables;  // [grid][hcap] when the table is global
+  // standard policy, per-query mode: an exact visited BITMAP indexed by node
+  // id, bm_words u32 per resident CTA (cleared per query), instead of the
+  // hashed table — one L2 atomicOr per candidate, no probing, never full
+  uint32_t* bitmaps;
+  uint32_t bm_words;
   uint32_t* gens;               // [grid]
   uint32_t* work;               // query counter
   uint32_t* out_ids;
@@ -642,6 +647,7 @@ search_kernel(const KParams P) {
   uint32_t tag = SMEM_TABLE ? 0 : P.gens[blockIdx.x];
   const uint32_t mask = P.hcap - 1;
   const bool forget = P.policy == 1;
+  uint32_t* const bm = P.bitmaps ? P.bitmaps + (size_t)blockIdx.x * P.bm_words : nullptr;
 
   for (;;) {
     if (tid == 0) ctl.qi = atomicAdd(P.work, 1u);
@@ -653,6 +659,10 @@ search_kernel(const KParams P) {
     for (uint32_t i = tid; i < P.ld; i += SNT) S.q[i] = P.queries[(size_t)qreal * P.ld + i];
     for (uint32_t i = tid; i < P.M; i += SNT) S.topA[i] = kDummyKey;
     if (SMEM_TABLE) smem_table_clear(S.table, P.hcap);
+    if (bm) {  // the previous query's marks (bm_words is a multiple of 4)
+      uint4* b4 = reinterpret_cast<uint4*>(bm);
+      for (uint32_t i = tid; i < (P.bm_words >> 2); i += SNT) b4[i] = make_uint4(0, 0, 0, 0);
+    }
     if (!SMEM_TABLE && P.mc_teams) {
       gtab = P.gtables + (size_t)qreal * P.hcap;  // shared by the query's teams
       tag = P.mc_tag;
@@ -735,17 +745,35 @@ search_kernel(const KParams P) {
               }
             }
           }
+          if (bm) {
+            // visited bitmap (standard policy): the word returned by atomicOr
+            // names the one winner; all VPT atomics in flight before any use
+            uint32_t old[VPT];
 #pragma unroll
-          for (int k = 0; k < VPT; ++k) {
-            const uint32_t j = j0 + k * SNT + tid;
-            if (j0 + k * SNT >= cnt) break;
-            bool ins = false;
-            if (j < cnt)
-              ins = SMEM_TABLE ? smem_insert(S.table, mask, ids[k])
-                  : P.mc_teams ? smem_insert(P.mc_tab + (size_t)qreal * P.hcap, mask, ids[k])
-                               : gtab_insert(gtab, mask, tag, ids[k]);
-            const uint32_t pos = warp_append_slot(&ctl.nev, ins);
-            if (ins) S.evlist[pos] = ids[k];
+            for (int k = 0; k < VPT; ++k) {
+              const uint32_t j = j0 + k * SNT + tid;
+              old[k] = j < cnt ? atomicOr(bm + (ids[k] >> 5), 1u << (ids[k] & 31)) : ~0u;
+            }
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+              if (j0 + k * SNT >= cnt) break;
+              const bool ins = !((old[k] >> (ids[k] & 31)) & 1u);
+              const uint32_t pos = warp_append_slot(&ctl.nev, ins);
+              if (ins) S.evlist[pos] = ids[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+              const uint32_t j = j0 + k * SNT + tid;
+              if (j0 + k * SNT >= cnt) break;
+              bool ins = false;
+              if (j < cnt)
+                ins = SMEM_TABLE ? smem_insert(S.table, mask, ids[k])
+                    : P.mc_teams ? smem_insert(P.mc_tab + (size_t)qreal * P.hcap, mask, ids[k])
+                                 : gtab_insert(gtab, mask, tag, ids[k]);
+              const uint32_t pos = warp_append_slot(&ctl.nev, ins);
+              if (ins) S.evlist[pos] = ids[k];
+            }
           }
         }
         __syncthreads();
@@ -1467,6 +1495,12 @@ KernelFn shared_fn(bool exact, Variant v) {
 
 }  // namespace
 
+// CAGRA_VISITED_BITMAP=0: the hashed generation-tagged table instead (A/B)
+bool bitmap_disabled() {
+  const char* e = std::getenv("CAGRA_VISITED_BITMAP");
+  return e && e[0] == '0';
+}
+
 uint64_t mc_table_bytes_per_query(const SearchConfig& c, uint32_t degree) {
   // the shared-mode visited table of plan_search (engine.cpp:47-50)
   const uint32_t imax = resolved_max_iter(c.max_iter, c.topm, 1);
@@ -1556,6 +1590,12 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
       throw UsageErr("search: multi-CTA visited tables exceed the device memory budget");
     pl.table_elems = (uint64_t)nq * hcap;
     pl.team_elems = (uint64_t)nq * T * c.topm;
+  } else if (!pl.smem_table && !forget && !shared_mode && !bitmap_disabled() &&
+             grid * (uint64_t)round_up_u32((ix.n + 31) / 32, 4) * 4 <= table_budget) {
+    // exact visited bitmap per resident CTA (n bits: 125 KB at 1M points)
+    pl.bitmap = true;
+    pl.bm_words = round_up_u32((ix.n + 31) / 32, 4);
+    pl.table_elems = (grid * (uint64_t)pl.bm_words + 1) / 2;
   } else if (!pl.smem_table) {
     uint64_t per = hcap * 8;
     uint64_t maxg = table_budget / per;
@@ -1638,6 +1678,8 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
   P.seed_mode = c.seed_mode;
   P.gtables = d_tables;
   P.gens = d_gens;
+  P.bitmaps = pl.bitmap ? reinterpret_cast<uint32_t*>(d_tables) : nullptr;
+  P.bm_words = pl.bm_words;
   P.work = d_work;
   P.out_ids = d_ids;
   P.out_dists = d_dists;
