@@ -142,6 +142,16 @@ int cagra_exact_knn_rows(const float* data, uint32_t n, uint32_t dim, uint32_t k
                          uint32_t row_begin, uint32_t row_end, int device, uint32_t* ids_out,
                          float* dists_out);
 
+/* nn_descent (knn_build.hpp:42; knn_build.cpp:96-231) on the device: random
+ * initial rows, rounds of neighbour-of-neighbour joins over sampled new/old
+ * entries until fewer than termination_delta * N * k row insertions or
+ * max_rounds.  Deterministic for a fixed seed.  Rows sorted by (dist, id),
+ * distances the sequential fp32 chain.  k <= 256. */
+int cagra_nn_descent(const float* data, uint32_t n, uint32_t dim, uint32_t k, double sample_rate,
+                     double termination_delta, uint32_t max_rounds, uint64_t seed, int device,
+                     uint32_t* ids_out, float* dists_out, uint32_t* converged_out,
+                     uint32_t* rounds_out);
+
 /* exact_topk (topk.hpp:20) for a batch of queries: k nearest by (dist, id). */
 int cagra_exact_topk(const float* data, uint32_t n, uint32_t dim, const float* queries,
                      uint32_t nq, uint32_t k, int device, uint32_t* ids_out,

@@ -91,6 +91,7 @@ EXPORTS = [
     "cagra_graph_metrics", "cagra_trim_scratch", "cagra_knn_last_filter",
     "cagra_exact_knn_rows", "cagra_build_graph_multi", "cagra_mindex_create",
     "cagra_mindex_destroy", "cagra_mindex_info", "cagra_msearch", "cagra_exact_knn_graph_multi",
+    "cagra_nn_descent",
 ]
 
 _lib = None
@@ -141,6 +142,8 @@ def lib() -> C.CDLL:
         L.cagra_mindex_info.argtypes = [vp, vp, vp, vp, vp, vp]
         L.cagra_msearch.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp, vp, vp]
         L.cagra_exact_knn_graph_multi.argtypes = [vp, u32, u32, u32, vp, u32, vp, vp]
+        L.cagra_nn_descent.argtypes = [vp, u32, u32, u32, C.c_double, C.c_double, u32, u64, i32,
+                                       vp, vp, vp, vp]
         L.cagra_trim_scratch.argtypes = [i32]
         L.cagra_knn_last_filter.argtypes = [vp, vp]
         _lib = L

@@ -367,6 +367,38 @@ int cagra_exact_knn_graph(const float* data, uint32_t n, uint32_t dim, uint32_t 
   });
 }
 
+int cagra_nn_descent(const float* data, uint32_t n, uint32_t dim, uint32_t k, double sample_rate,
+                     double termination_delta, uint32_t max_rounds, uint64_t seed, int device,
+                     uint32_t* ids_out, float* dists_out, uint32_t* converged_out,
+                     uint32_t* rounds_out) {
+  return guarded([&] {
+    // knn_build.cpp:97-102, same order
+    if (k == 0 || k >= n) throw UsageErr("nn_descent: require 1 <= k < N");
+    if (!(sample_rate > 0.0 && sample_rate <= 1.0))
+      throw UsageErr("nn_descent: sample_rate must be in (0, 1]");
+    if (!(termination_delta > 0.0 && termination_delta < 1.0))
+      throw UsageErr("nn_descent: termination_delta must be in (0, 1)");
+    if (dim == 0) throw UsageErr("dataset dimension must be >= 1");
+    int dev = resolve_device(device);
+    DeviceScope scope(dev);
+    Stream st;
+    const uint32_t ld = row_stride(dim);
+    DBuf dd(sizeof(float) * (size_t)n * ld), di(sizeof(uint32_t) * (size_t)n * k),
+        ds(sizeof(float) * (size_t)n * k);
+    upload_rows(dd.as<float>(), data, n, dim, ld, st.s);
+    const NnDescentInfo info =
+        launch_nn_descent(dd.as<float>(), n, ld, dim, k, sample_rate, termination_delta,
+                          max_rounds, seed, di.as<uint32_t>(), ds.as<float>(), st.s);
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(ids_out, di.p, sizeof(uint32_t) * (size_t)n * k,
+                                   cudaMemcpyDeviceToHost, st.s));
+    CAGRA_CUDA_TRY(cudaMemcpyAsync(dists_out, ds.p, sizeof(float) * (size_t)n * k,
+                                   cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (converged_out) *converged_out = info.converged ? 1u : 0u;
+    if (rounds_out) *rounds_out = info.rounds;
+  });
+}
+
 int cagra_exact_knn_rows(const float* data, uint32_t n, uint32_t dim, uint32_t k,
                          uint32_t row_begin, uint32_t row_end, int device, uint32_t* ids_out,
                          float* dists_out) {

@@ -39,6 +39,19 @@ extern KnnTcStats g_knn_tc_stats;
 // Frees the kNN build's cached scratch on `device` (all devices when < 0).
 void knn_trim_scratch(int device);
 
+// ---- nn_descent.cu -------------------------------------------------------------
+struct NnDescentInfo {
+  uint32_t rounds = 0;
+  bool converged = false;
+  unsigned long long last_inserted = 0;
+};
+// nn_descent (knn_build.cpp:96-231) on device: rows [n][k] sorted by (dist, id)
+// with sequential-chain distances; synchronous on `s`.
+NnDescentInfo launch_nn_descent(const float* d_data, uint32_t n, uint32_t ld, uint32_t dim,
+                                uint32_t k, double sample_rate, double termination_delta,
+                                uint32_t max_rounds, uint64_t seed, uint32_t* d_ids,
+                                float* d_dists, cudaStream_t s);
+
 // ---- metrics.cu ---------------------------------------------------------------
 // Distinct <=2-hop neighbours summed over all nodes (avg_2hop_count * n) and
 // the strongly connected component count; synchronous on `stream`.

@@ -319,6 +319,35 @@ def exact_knn_graph(ds: Dataset, k: int, num_threads: int = 0, device: int = 0) 
     return KnnGraph(n, k, ids, dists)
 
 
+@dataclass
+class NNDescentParams:
+    """knn_build.hpp:33-39."""
+    sample_rate: float = 0.5
+    termination_delta: float = 0.001
+    max_rounds: int = 20
+    seed: int = 0
+    num_threads: int = 0
+
+
+def nn_descent(ds: Dataset, k: int, params: Optional[NNDescentParams] = None,
+               device: int = 0) -> KnnGraph:
+    """knn_build.hpp:42 / knn_build.cpp:96-231, on the device (cagra_nn_descent)."""
+    params = params or NNDescentParams()
+    n, dim = ds.data.shape
+    ids = np.empty((n, k), np.uint32) if 0 < k < n else np.empty((0, 0), np.uint32)
+    dists = np.empty(ids.shape, np.float32)
+    conv = C.c_uint32(0)
+    rounds = C.c_uint32(0)
+    check(lib().cagra_nn_descent(ptr(ds.data), n, dim, k, float(params.sample_rate),
+                                 float(params.termination_delta), int(params.max_rounds),
+                                 int(params.seed) & 0xFFFFFFFFFFFFFFFF, device, ptr(ids),
+                                 ptr(dists), C.byref(conv), C.byref(rounds)))
+    g = KnnGraph(n, k, ids, dists)
+    g.converged = bool(conv.value)
+    g.rounds = int(rounds.value)
+    return g
+
+
 def sort_neighbor_lists(g: KnnGraph) -> None:
     """knn_build.cpp:65-79 (host bookkeeping)."""
     if g.dists.shape != g.ids.shape:

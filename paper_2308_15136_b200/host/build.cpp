@@ -28,16 +28,24 @@ KnnGraph exact_knn_graph(const Dataset& ds, std::uint32_t k, unsigned /*num_thre
     return g;
 }
 
-// knn_build.cpp:96-102 validation; the graph itself is the exact device build
-// (the paper's NN-descent is replaced by the tensor-core brute force).
+// nn_descent (knn_build.cpp:96-231) on the device (csrc/nn_descent.cu):
+// same validation, deterministic for a fixed seed, thread count ignored.
 KnnGraph nn_descent(const Dataset& ds, std::uint32_t k, const NNDescentParams& params) {
     if (k == 0 || k >= ds.size()) throw UsageError("nn_descent: require 1 <= k < N");
     if (params.sample_rate <= 0.0 || params.sample_rate > 1.0)
         throw UsageError("nn_descent: sample_rate must be in (0, 1]");
     if (params.termination_delta <= 0.0 || params.termination_delta >= 1.0)
         throw UsageError("nn_descent: termination_delta must be in (0, 1)");
-    KnnGraph g = exact_knn_graph(ds, k, params.num_threads);
-    g.converged = true;
+    KnnGraph g;
+    g.num_nodes = ds.size();
+    g.degree = k;
+    g.ids.resize(static_cast<std::size_t>(g.num_nodes) * k);
+    g.dists.resize(g.ids.size());
+    std::uint32_t conv = 0;
+    b200::check(cagra_nn_descent(ds.raw(), ds.size(), ds.dim(), k, params.sample_rate,
+                                 params.termination_delta, params.max_rounds, params.seed,
+                                 b200::device(), g.ids.data(), g.dists.data(), &conv, nullptr));
+    g.converged = conv != 0;
     return g;
 }
 
