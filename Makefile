@@ -17,7 +17,7 @@ FODG    := $(PKG)/lib/libfodg_b200.so
 
 CLI     := $(PKG)/lib/fodg
 
-all: $(LIB) $(if $(HOST_SRC),$(FODG)) $(CLI) oracle refsuite
+all: $(LIB) $(if $(HOST_SRC),$(FODG)) $(CLI) oracle refsuite tools
 
 build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/kernels.hpp $(PKG)/csrc/host_util.hpp include/cagra/capi.h
 	@mkdir -p build
@@ -56,10 +56,17 @@ refsuite:
 	@echo "refsuite: /root/reference absent; using prebuilt tests/_refsuite if any"
 endif
 
+# measurement tools (C++ callers of the C ABI / the drop-in; not part of the product)
+TOOLS := tools/cpp/b1_latency tools/cpp/dropin_bench
+tools: $(TOOLS)
+tools/cpp/%: tools/cpp/%.cpp $(FODG)
+	g++ -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG)/lib -lfodg_b200 -lcagra_b200 \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
 	rm -rf build $(PKG)/lib
 
-.PHONY: all oracle clean refsuite
+.PHONY: all oracle clean refsuite tools
