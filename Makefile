@@ -17,7 +17,7 @@ FODG    := $(PKG)/lib/libfodg_b200.so
 
 CLI     := $(PKG)/lib/fodg
 
-all: $(LIB) $(if $(HOST_SRC),$(FODG)) $(CLI) oracle refsuite tools
+all: $(LIB) $(if $(HOST_SRC),$(FODG)) $(CLI) oracle refsuite tools dropintests
 
 build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/kernels.hpp $(PKG)/csrc/host_util.hpp include/cagra/capi.h
 	@mkdir -p build
@@ -56,6 +56,14 @@ refsuite:
 	@echo "refsuite: /root/reference absent; using prebuilt tests/_refsuite if any"
 endif
 
+# drop-in behaviour tests (C++ callers of fodg::, run by tests/test_dropin.py)
+DROPIN_TESTS := tests/_dropin/test_dropin_cache
+dropintests: $(DROPIN_TESTS)
+tests/_dropin/%: tests/cpp/%.cpp $(FODG)
+	@mkdir -p tests/_dropin
+	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG)/lib -lfodg_b200 -lcagra_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
+
 # measurement tools (C++ callers of the C ABI / the drop-in; not part of the product)
 TOOLS := tools/cpp/b1_latency tools/cpp/dropin_bench
 tools: $(TOOLS)
@@ -69,4 +77,4 @@ oracle:
 clean:
 	rm -rf build $(PKG)/lib
 
-.PHONY: all oracle clean refsuite tools
+.PHONY: all oracle clean refsuite tools dropintests

@@ -52,7 +52,7 @@ std::vector<int> devices() {
 
 bool fast_distances() {
     const char* e = std::getenv("CAGRA_FAST_DISTANCES");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
 }
 
 unsigned device_sm_count() {
@@ -183,6 +183,72 @@ CacheEntry& entry_for(const Graph& graph, const Dataset& ds, const std::vector<i
 cagra_index* index_for(const Graph& graph, const Dataset& ds) {
     std::lock_guard<std::mutex> lock(g_mu);
     return entry_for(graph, ds, {device()}).ix;
+}
+
+void with_index(const Graph& graph, const Dataset& ds,
+                const std::function<void(cagra_index*, cagra_mindex*)>& search) {
+    const std::vector<int> devs = devices();
+    if (trust_identity()) {
+        cagra_index* ix = nullptr;
+        cagra_mindex* mx = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(g_mu);
+            CacheEntry& e = entry_for(graph, ds, devs);
+            ix = e.ix;
+            mx = e.mx;
+        }
+        search(ix, mx);
+        return;
+    }
+    // a copy matching by address and shape is searched while its contents are
+    // re-hashed on host threads (the previous hashes are in the entry)
+    cagra_index* ix = nullptr;
+    cagra_mindex* mx = nullptr;
+    std::uint64_t want_d = 0, want_i = 0;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+            if (it->data == ds.raw() && it->ids == graph.ids.data() && it->n == ds.size() &&
+                it->dim == ds.dim() && it->degree == graph.degree && it->devs == devs) {
+                g_cache.splice(g_cache.begin(), g_cache, it);
+                ix = it->ix;
+                mx = it->mx;
+                want_d = it->h_data;
+                want_i = it->h_ids;
+                break;
+            }
+        }
+    }
+    if (ix || mx) {
+        std::uint64_t hd = 0, hi = 0;
+        std::thread hasher([&] {
+            hd = content_hash(ds.raw(), 4ull * ds.size() * ds.dim());
+            hi = content_hash(graph.ids.data(), 4ull * graph.ids.size());
+        });
+        try {
+            search(ix, mx);
+        } catch (...) {
+            hasher.join();
+            throw;
+        }
+        hasher.join();
+        if (hd == want_d && hi == want_i) return;
+        // contents changed in place: drop the stale copy, upload, search again
+        std::lock_guard<std::mutex> lock(g_mu);
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+            if (it->ix == ix && it->mx == mx) {
+                destroy(*it);
+                g_cache.erase(it);
+                break;
+            }
+    }
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        CacheEntry& e = entry_for(graph, ds, devs);
+        ix = e.ix;
+        mx = e.mx;
+    }
+    search(ix, mx);
 }
 
 cagra_mindex* mindex_for(const Graph& graph, const Dataset& ds) {

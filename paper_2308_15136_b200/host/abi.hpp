@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "cagra/capi.h"
@@ -26,14 +27,24 @@ int device();
 std::vector<int> devices();
 
 /// Fast in-loop distances (team reductions; reported distances still the
-/// sequential chain) instead of the reference-order chain everywhere.  Off by
-/// default so the drop-in reproduces the reference bit for bit; env
-/// CAGRA_FAST_DISTANCES=1 turns it on.
+/// sequential chain, ids and recall as the reference's within the parity bar)
+/// — the default; CAGRA_FAST_DISTANCES=0 selects the reference-order chain
+/// everywhere (ids, distances and counters bit for bit).
 bool fast_distances();
 
 /// The device index for (graph, ds), created on first use and reused while
 /// the host buffers are unchanged.
 cagra_index* index_for(const Graph& graph, const Dataset& ds);
+
+/// Runs `search(ix, mx)` on the cached device copy of (graph, ds) for the
+/// current device set (one of ix / mx is set).  A cached copy found by
+/// address and shape is searched at once while the full-content hash of the
+/// host buffers is computed on host threads in parallel; if the contents
+/// changed, the copy is re-uploaded and the search re-run — so in-place edits
+/// are always seen, and the check costs no latency when the search takes
+/// longer than the hash (large batches).
+void with_index(const Graph& graph, const Dataset& ds,
+                const std::function<void(cagra_index*, cagra_mindex*)>& search);
 
 /// The replicated device-set index (CAGRA_DEVICES with more than one entry)
 /// for (graph, ds), cached under the same rule as index_for.

@@ -49,11 +49,6 @@ std::vector<SearchResult> batch_search(const Graph& graph, const Dataset& ds, co
     if (options.mode == ExecutionMode::kSharedQueryWorkers && options.team_count < 2)
         throw UsageError("batch_search: shared mode requires team_count >= 2");
     if (graph.num_nodes != ds.size()) throw UsageError("search: graph/dataset size mismatch");
-    // CAGRA_DEVICES=0,1,...: the batch is split over replicas on those GPUs
-    // (results identical to one device: every query keeps its global seed)
-    const bool multi = b200::devices().size() > 1;
-    cagra_index* ix = multi ? nullptr : b200::index_for(graph, ds);
-    cagra_mindex* mx = multi ? b200::mindex_for(graph, ds) : nullptr;
     const cagra_search_params p = to_abi(params);
     cagra_engine_opts o;
     cagra_engine_opts_default(&o);
@@ -66,12 +61,16 @@ std::vector<SearchResult> batch_search(const Graph& graph, const Dataset& ds, co
     std::vector<std::uint32_t> ids(static_cast<std::size_t>(nq) * k), counts(nq);
     std::vector<float> dists(ids.size());
     std::vector<cagra_search_stats> st(nq);
-    if (multi)
-        b200::check(cagra_msearch(mx, queries.raw(), nq, queries.dim(), &p, &o, ids.data(),
-                                  dists.data(), counts.data(), st.data()));
-    else
-        b200::check(cagra_search(ix, queries.raw(), nq, queries.dim(), &p, &o, ids.data(),
-                                 dists.data(), counts.data(), st.data()));
+    // CAGRA_DEVICES=0,1,...: the batch is split over replicas on those GPUs
+    // (results identical to one device: every query keeps its global seed)
+    b200::with_index(graph, ds, [&](cagra_index* ix, cagra_mindex* mx) {
+        if (mx)
+            b200::check(cagra_msearch(mx, queries.raw(), nq, queries.dim(), &p, &o, ids.data(),
+                                      dists.data(), counts.data(), st.data()));
+        else
+            b200::check(cagra_search(ix, queries.raw(), nq, queries.dim(), &p, &o, ids.data(),
+                                     dists.data(), counts.data(), st.data()));
+    });
     std::vector<SearchResult> out(nq);
     for (std::uint32_t q = 0; q < nq; ++q) {
         auto& r = out[q];

@@ -38,9 +38,14 @@ def test_reference_host_suite(suite):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("distances", ["fast", "reference-order"])
 @pytest.mark.parametrize("suite", [s for s in SUITES if s not in HOST_ONLY])
-def test_reference_unit_suite_on_b200(gpu, suite):
-    r = _run(_bin(suite))
+def test_reference_unit_suite_on_b200(gpu, suite, distances):
+    # the drop-in's default (team-reduced in-loop distances, reported distances
+    # re-scored with the sequential chain) and CAGRA_FAST_DISTANCES=0 (the
+    # reference-order chain everywhere) both pass the reference's own suites
+    env = dict(os.environ, CAGRA_FAST_DISTANCES="1" if distances == "fast" else "0")
+    r = _run(_bin(suite), env=env)
     summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest-compat]")]
     assert summary, r.stdout + r.stderr
     assert r.returncode == 0, summary[0] + "\n" + r.stderr[-4000:]
