@@ -44,7 +44,7 @@ def launches(src, dst):
     print("\n".join(lines))
 
 
-def full(rep, dst, key, alg, label):
+def full(rep, dst, key, alg, label, command=None):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
@@ -78,12 +78,15 @@ def full(rep, dst, key, alg, label):
             "grid": val("launch__grid_size"), "block": val("launch__block_size"),
             "sm_throughput_pct": val("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
         })
+        if "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active" in d:
+            res[-1]["tensor_pipe_active_pct"] = val(
+                "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
     top = res[0]
     top.update({"config_key": key, "label": label, "source": rep,
                 "algorithmic_bytes_per_launch": alg,
-                "command": "ncu --set full --clock-control none --import-source on "
-                           "-k regex:search_kernel -s 3 -c 1 python bench.py --steps 1 "
-                           "--warmup 3 --no-cpu"})
+                "command": command or ("ncu --set full --clock-control none --import-source on "
+                                       "-k regex:search_kernel -s 3 -c 1 python bench.py "
+                                       "--steps 1 --warmup 3 --no-cpu")})
     json.dump(top, open(dst, "w"), indent=1)
     print(json.dumps(top, indent=1))
 
@@ -95,4 +98,4 @@ if __name__ == "__main__":
         a = sys.argv[4:]
         kw = dict(zip(a[0::2], a[1::2]))
         full(sys.argv[2], sys.argv[3], kw.get("--config-key", ""),
-             float(kw.get("--alg-bytes", "0")), kw.get("--label", ""))
+             float(kw.get("--alg-bytes", "0")), kw.get("--label", ""), kw.get("--command"))
