@@ -149,6 +149,24 @@ __device__ __forceinline__ float seq_step(float acc, float a, float b) {
   float diff = __fsub_rn(a, b);
   return __fadd_rn(acc, __fmul_rn(diff, diff));
 }
+// The sequential chain over a whole row (squared_l2, dataset.hpp:38-41) with
+// 128-bit loads: rows are 16-byte aligned with a stride that is a multiple of
+// 4 floats; the additions stay in index order, so the result is bit-equal.
+__device__ __forceinline__ float seq_dist(const float* __restrict__ x, const float* __restrict__ q,
+                                          uint32_t dim) {
+  float acc = 0.0f;
+  uint32_t i = 0;
+  for (; i + 4 <= dim; i += 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(x + i));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(q + i));
+    acc = seq_step(acc, a.x, b.x);
+    acc = seq_step(acc, a.y, b.y);
+    acc = seq_step(acc, a.z, b.z);
+    acc = seq_step(acc, a.w, b.w);
+  }
+  for (; i < dim; ++i) acc = seq_step(acc, __ldg(x + i), __ldg(q + i));
+  return acc;
+}
 #endif
 
 // ---- host-side error types; capi.cu maps them to status codes ----
