@@ -619,8 +619,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tau_f = key_dist(tau);
       tau_e = tau_e_of(tau_f);
     };
+#if !CAGRA_TC_STAGED_APPEND
     // append mode: each lane owns its row's global buffer (no staging)
     uint64_t* const row_buf = P.mode == 1 && live ? P.bufs + (size_t)row * P.capg : nullptr;
+#endif
     // slow path of one 32-column chunk: only the FMNMX3 groups whose minimum
     // passes are examined element by element (appends are rare after the
     // first tiles); warp-uniform entry (the pending-buffer check is a vote)
