@@ -87,6 +87,10 @@ def parse():
     ap.add_argument("--hash", default="forgettable", choices=["standard", "forgettable"])
     ap.add_argument("--hash-bits", type=int, default=12)
     ap.add_argument("--shard", default="query", choices=["query", "data"])
+    ap.add_argument("--data", default="uniform", choices=["uniform", "lowrank"],
+                    help="synthetic generator: the reference fixture's uniform[0,1) "
+                         "(default) or low-intrinsic-dimension rows (C3)")
+    ap.add_argument("--rank", type=int, default=32, help="intrinsic dimension for --data lowrank")
     ap.add_argument("--shards-per-rank", type=int, default=1,
                     help="data-sharded: id-range shards held by each rank (C5 on one GPU: 8)")
     ap.add_argument("--cpu-sample", type=int, default=0,
@@ -240,16 +244,40 @@ def relaunch(args):
 
 
 # ------------------------------------------------------------ shared inputs --
-def make_inputs(args, world, rank):
+def lowrank_dataset(n, dim, rank, seed):
+    """Low-intrinsic-dimension synthetic rows (the C3 decision):
+    x = z A + e with z ~ U[0,1)^rank per row, one fixed A ~ U[-0.5,0.5)^(rank x
+    dim) and e ~ 0.01 U[0,1)^dim (numpy PCG64; A from seed 4242, z / e from
+    `seed`).  Uniform 960-d data has no neighbourhood structure (recall
+    saturates near 0.8 for both arms); this keeps the GIST shape with a
+    structure graph search can use.  Both arms search the same arrays."""
+    a = np.random.default_rng(4242).random((rank, dim), dtype=np.float32) - np.float32(0.5)
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, dim), np.float32)
+    step = 1 << 18
+    for i in range(0, n, step):
+        m = min(step, n - i)
+        z = rng.random((m, rank), dtype=np.float32)
+        out[i:i + m] = z @ a + np.float32(0.01) * rng.random((m, dim), dtype=np.float32)
+    return out
+
+
+def gen_rows(args, count, seed):
     from paper_2308_15136_b200 import capi
 
-    data = capi.uniform_dataset(args.n, args.dim, 424242)
+    if args.data == "lowrank":
+        return lowrank_dataset(count, args.dim, args.rank, seed)
+    return capi.uniform_dataset(count, args.dim, seed)
+
+
+def make_inputs(args, world, rank):
+    data = gen_rows(args, args.n, 424242)
     if args.shard == "data":
-        queries = capi.uniform_dataset(args.batch, args.dim, 424243)
+        queries = gen_rows(args, args.batch, 424243)
         return data, queries
     # every rank owns its own batch of queries (weak scaling); rank 0's batch is
     # the single-GPU batch
-    allq = capi.uniform_dataset(args.batch * world, args.dim, 424243)
+    allq = gen_rows(args, args.batch * world, 424243)
     queries = np.ascontiguousarray(allq[rank * args.batch:(rank + 1) * args.batch])
     return data, queries
 
@@ -625,7 +653,10 @@ def run_query_sharded(args, D):
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (reference fixture generator mt19937_64 uniform[0,1))",
+            "data": ("synthetic (reference fixture generator mt19937_64 uniform[0,1))"
+                     if args.data == "uniform" else
+                     f"synthetic low-rank: z A + 0.01 e, intrinsic dimension {args.rank} "
+                     "(numpy PCG64; bench.lowrank_dataset), same arrays for both arms"),
             "config": cfg,
             "value_is": "batch-10k QPS (per GPU batch) at recall@10 >= 0.95; batch 1 in `batch1`",
             "recall@10": rec_all,
@@ -804,8 +835,8 @@ def run_data_sharded(args, D):
     mine = list(range(rank * S, (rank + 1) * S))
     big = args.n > 20_000_000
     if not big:
-        full = capi.uniform_dataset(args.n, args.dim, 424242)
-    queries = capi.uniform_dataset(args.batch, args.dim, 424243)
+        full = gen_rows(args, args.n, 424242)
+    queries = gen_rows(args, args.batch, 424243)
     nq, k = args.batch, 10
     shards, build_s, knn_s, opt_s = [], 0.0, 0.0, 0.0
     gt_lists = []

@@ -23,10 +23,18 @@ def main():
     ap.add_argument("--nq", type=int, default=10_000)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--grid", default="")
+    ap.add_argument("--data", default="uniform", choices=["uniform", "lowrank"])
+    ap.add_argument("--rank", type=int, default=32)
     args = ap.parse_args()
     t = time.time()
-    data = capi.uniform_dataset(args.n, args.dim, 424242)
-    queries = capi.uniform_dataset(args.nq, args.dim, 424243)
+    if args.data == "lowrank":
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import lowrank_dataset
+        data = lowrank_dataset(args.n, args.dim, args.rank, 424242)
+        queries = lowrank_dataset(args.nq, args.dim, args.rank, 424243)
+    else:
+        data = capi.uniform_dataset(args.n, args.dim, 424242)
+        queries = capi.uniform_dataset(args.nq, args.dim, 424243)
     print(f"gen {time.time()-t:.1f}s", flush=True)
     ds = fodg.Dataset.from_array(data)
     t = time.time()
