@@ -679,6 +679,14 @@ def run_query_sharded(args, D):
         }
         if parity is not None:
             line["parity"] = parity
+        if cpu and cpu.get("mean_distance_evals") and args.cpu_hash == "standard" and \
+                args.cpu_topm == args.topm and args.cpu_width == args.width:
+            # the standard (never-forget) policy's evaluations at the same M, p:
+            # the share of this kernel's gathered rows that are not revisits
+            std_e = cpu["mean_distance_evals"]
+            line["roofline"]["standard_policy_mean_evals"] = std_e
+            line["roofline"]["useful_fraction_vs_standard"] = std_e / float(evals.mean())
+            line["roofline"]["frac_useful"] = line["roofline"]["frac"] * std_e / float(evals.mean())
         if b1 is not None:
             line["batch1"] = b1
         if opt_par is not None:
@@ -717,11 +725,12 @@ def cpu_batch_legs(args, data, graph, queries, gt, gpu_ids):
     sample = args.cpu_sample or int(min(args.batch, max(threads, 10.0 / max(per_q, 1e-6))))
     sample = max(1, min(sample, args.batch))
     t0 = time.perf_counter()
-    ids, _, _, _ = rix.batch_search(queries[:sample], pb, threads=threads)
+    ids, _, _, st = rix.batch_search(queries[:sample], pb, threads=threads)
     el = time.perf_counter() - t0
     rix.close()
     cpu = {"value": sample / el, "unit": "queries/s", "cores": threads, "kind": "reference",
            **host_cpu(), "recall@10": recall_at_k(ids, gt[:sample]),
+           "mean_distance_evals": float(np.mean(st["distance_evals"])),
            "operating_point": f"per-query M={args.cpu_topm} p={args.cpu_width} {args.cpu_hash} "
                               "hash (default: the reference's best recall>=0.95 grid point at "
                               "1M x 96, profiles/r02_cpu_batch10k_sweep.txt)",

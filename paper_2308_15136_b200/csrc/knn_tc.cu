@@ -79,6 +79,16 @@ constexpr uint32_t TC_A_COL = 2 * 128;         // TS: A at TMEM columns [256, 25
 constexpr int TC_MAX_KB = 8;  // K <= 512 keeps the query tile resident
 constexpr int TC_MAX_KB_STREAM = 64;  // beyond: query tile streamed with each data tile (SA)
 constexpr uint32_t TILE_BYTES = TC_BN * TC_BK * 2;  // 16 KB
+constexpr uint32_t BOX_ROWS = 64;                   // B tensor-map box: 64 points x 64 K
+constexpr uint32_t BOX_BYTES = BOX_ROWS * TC_BK * 2;  // 8 KB
+// Option: two-half CTAs stream 64-point data tiles into 4 accumulators per half
+// (TMEM 2 x 4 x 64 columns): the MMA can run up to 3 tiles ahead of the
+// epilogue instead of 1 (the epilogue's per-tile latency varies with its
+// appends). Measured slower on 1M x 96 k=128 (0.60 s vs 0.404 s: twice the
+// per-tile barrier and release work), so 128-point tiles stay the default.
+#ifndef CAGRA_TC_W64
+#define CAGRA_TC_W64 0
+#endif
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -244,11 +254,9 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | (uint64_t)(1024u >> 4) << 32 | 1ull << 46 |
          2ull << 61;
 }
-// Instruction descriptor: fp32 accumulate, both operands K-major, M=128,
-// N=128; the A/B format bits (7-9, 10-12: 0 = f16, 1 = bf16) are OR-ed in at
-// run time.
-constexpr uint32_t kIdescShape = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) |
-                                 ((uint32_t)(TC_BM >> 4) << 24);
+// Instruction descriptor (built in the kernel): fp32 accumulate, both
+// operands K-major, M=128 (256 for a pair), N = the tile width; the A/B format
+// bits (7-9, 10-12: 0 = f16, 1 = bf16) are OR-ed in at run time.
 
 struct TcArgs {
   uint32_t nq, n, kblocks, KC, exclude_self, stages, pend_cap;
@@ -315,14 +323,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   constexpr uint32_t ROWS = TC_BM * HV;  // query rows per CTA
   // SA data tiles are 256 points wide (one N=256 MMA per k-block), so every
   // streamed A k-block is used against two 128-point B tiles
-  constexpr uint32_t W = SA ? 2 * TC_BN : TC_BN;  // data points per tile
-  constexpr int ACC = TS || SA || HV == 2 ? 2 : 4;  // W-column accumulators per half (512 cols)
-  constexpr uint32_t BTILE = PAIR ? TILE_BYTES / 2 : TILE_BYTES;  // B bytes per stage per CTA
-  constexpr uint32_t STAGE = SA ? 3 * TILE_BYTES : BTILE;         // [A k-block |] B k-block(s)
+  constexpr uint32_t W = SA ? 2 * TC_BN : (HV == 2 && CAGRA_TC_W64 ? 64u : (uint32_t)TC_BN);
+  constexpr int ACC = TS || SA ? 2 : (HV == 2 ? (W == 64 ? 4 : 2) : 4);  // per half (512 cols)
+  constexpr uint32_t BTILE = PAIR ? TILE_BYTES / 2 : W * TC_BK * 2;  // B bytes per stage per CTA
+  constexpr uint32_t STAGE = SA ? 3 * TILE_BYTES : BTILE;            // [A k-block |] B k-block(s)
   constexpr uint32_t idesc_shape =
       PAIR ? ((1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24))
-      : SA ? ((1u << 4) | ((uint32_t)(W >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24))
-           : kIdescShape;
+           : ((1u << 4) | ((uint32_t)(W >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24));
   const uint32_t idesc = idesc_shape | (P.ab_fmt << 7) | (P.ab_fmt << 10);
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B tiles
@@ -420,14 +427,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             // back to back (one K-major SWIZZLE_128B operand of 256 rows)
             mbar_expect_tx(full0 + 8 * s, 3 * TILE_BYTES);
             tma_load_2d(smem_u32(sB + s * STAGE), &tmA, full0 + 8 * s, kb * TC_BK, row0);
-            tma_load_2d(smem_u32(sB + s * STAGE + TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
-                        tile_of(t) * W);
-            tma_load_2d(smem_u32(sB + s * STAGE + 2 * TILE_BYTES), &tmB, full0 + 8 * s,
-                        kb * TC_BK, tile_of(t) * W + TC_BN);
+#pragma unroll
+            for (uint32_t b = 0; b < W / BOX_ROWS; ++b)  // 64-point boxes back to back
+              tma_load_2d(smem_u32(sB + s * STAGE + TILE_BYTES + b * BOX_BYTES), &tmB,
+                          full0 + 8 * s, kb * TC_BK, tile_of(t) * W + b * BOX_ROWS);
           } else {
-            mbar_expect_tx(full0 + 8 * s, TILE_BYTES);
-            tma_load_2d(smem_u32(sB + s * TILE_BYTES), &tmB, full0 + 8 * s, kb * TC_BK,
-                        tile_of(t) * TC_BN);
+            mbar_expect_tx(full0 + 8 * s, BTILE);
+#pragma unroll
+            for (uint32_t b = 0; b < W / BOX_ROWS; ++b)  // 64-point boxes back to back
+              tma_load_2d(smem_u32(sB + s * BTILE + b * BOX_BYTES), &tmB, full0 + 8 * s,
+                          kb * TC_BK, tile_of(t) * W + b * BOX_ROWS);
           }
         }
       }
@@ -1206,8 +1215,9 @@ size_t tc_smem_bytes(uint32_t kblocks, uint32_t stages, uint32_t pend_cap = TC_P
                      bool pair = false, uint32_t hv = 1) {
   const bool sa = tc_streamed(kblocks);
   const bool ts = CAGRA_KNN_TS && !pair && !sa && hv == 1;
-  const size_t stage = sa ? 3 * TILE_BYTES : (pair ? TILE_BYTES / 2 : TILE_BYTES);
-  const uint32_t acc = ts || sa || hv == 2 ? 2 : 4;
+  const bool w64 = hv == 2 && CAGRA_TC_W64;
+  const size_t stage = sa ? 3 * TILE_BYTES : (pair || w64 ? TILE_BYTES / 2 : TILE_BYTES);
+  const uint32_t acc = ts || sa ? 2 : (hv == 2 ? (w64 ? 4 : 2) : 4);
   return 1024 + (ts || sa ? 0 : (size_t)hv * kblocks * TILE_BYTES) + stages * stage +
          sizeof(uint64_t) * (pend_cap * TC_BM * hv + 2 * stages + 1 + 2 * acc) + 16;
 }
@@ -1217,7 +1227,7 @@ constexpr size_t kSmemLimit = 227 * 1024;
 // deepest B ring that fits next to the resident query tile
 uint32_t tc_stages(uint32_t kblocks, uint32_t pend_cap = TC_PEND, bool pair = false,
                    uint32_t hv = 1) {
-  uint32_t s = pair ? 2 * TC_STAGES : TC_STAGES;  // pair stages hold half tiles
+  uint32_t s = pair || (hv == 2 && CAGRA_TC_W64) ? 2 * TC_STAGES : TC_STAGES;  // half tiles
   while (s > 2 && tc_smem_bytes(kblocks, s, pend_cap, pair, hv) > kSmemLimit) --s;
   return s;
 }
@@ -1411,7 +1421,7 @@ void list_pass(const TcCall& c, const void* P, uint32_t nq, const float* qnorm,
   Dev lists(8ull * nq * KC * splits, c.stream), fails(4ull * nq + 4, c.stream), rer(8, c.stream);
   CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * nq + 4, c.stream));
   CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, c.stream));
-  const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
+  const uint32_t brows = BOX_ROWS;  // every B load is one or more 64-point boxes
   const bool f16 = c.terms == 1;
   CUtensorMap tmA = make_map(P, nq, c.Kp, 1, TC_BN, f16),
               tmB = make_map(c.R, c.n, c.Kp, 1, brows, f16);
@@ -1651,7 +1661,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     View lists1{arena(kSlotLists, 8ull * r * cmax)}, bufs{arena(kSlotBufs, 8ull * cmax * capg)},
         bcount{arena(kSlotBcount, 4ull * cmax)}, fails{arena(kSlotFails, 4ull * cmax + 4)},
         rer{arena(kSlotRer, 8)};
-    const uint32_t brows = tc_pair_enabled() && !tc_streamed(c.kblocks) ? TC_BN / 2 : TC_BN;
+    const uint32_t brows = BOX_ROWS;  // every B load is one or more 64-point boxes
     const bool f16 = c.terms == 1;
     CUtensorMap tmS = make_map(dR.p, ns, c.Kp, kSampleStride, brows, f16);
     CUtensorMap tmB = make_map(dR.p, n, c.Kp, 1, brows, f16);
