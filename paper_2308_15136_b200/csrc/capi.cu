@@ -240,8 +240,10 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
     grow(ix, ix->team_stats, sizeof(cagra_search_stats) * (size_t)nq * pl.teams);
     // per-query regions tagged by a call generation; a new layout starts clean
     const int kind = pl.b1 ? 2 : 1;
+    // (the fused kernel's regions are nq * hcap words: a new nq is a new layout,
+    // since each call clears the other region at the current layout)
     if (ix->mc_layout != kind || pl.hcap != ix->table_hcap || pl.table_elems > ix->table_elems ||
-        ix->mc_tag == 0xffffffffu) {
+        (pl.b1 && pl.grid != ix->table_grid) || ix->mc_tag == 0xffffffffu) {
       if (pl.table_elems > ix->table_elems) {
         grow(ix, ix->tables, sizeof(unsigned long long) * pl.table_elems);
         ix->table_elems = pl.table_elems;
@@ -249,7 +251,7 @@ void run_search(cagra_index* ix, const float* d_queries, uint32_t nq,
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->tables.p, 0, ix->tables.bytes, s));
       ix->mc_tag = 0;
       ix->table_hcap = pl.hcap;
-      ix->table_grid = 0;  // the per-CTA generations no longer match
+      ix->table_grid = pl.b1 ? pl.grid : 0;  // per-CTA generations no longer match
       grow(ix, ix->gens, sizeof(uint32_t) * std::max<uint32_t>(pl.grid, 1));
       CAGRA_CUDA_TRY(cudaMemsetAsync(ix->gens.p, 0, ix->gens.bytes, s));
       ix->mc_layout = kind;

@@ -123,6 +123,7 @@ struct SearchPlan {
   size_t init_elems = 0;   // u32 init sample ids
   bool mc = false;         // shared mode with one CTA per (query, team)
   bool b1 = false;         // mc via the fused small-team kernel (search_b1.cu)
+  bool b1_direct = false;  // its visited bitmap indexed by node id (hcap words >= n bits)
   bool bitmap = false;     // standard policy: exact visited bitmap per resident CTA
   uint32_t bm_words = 0;   // u32 words per CTA bitmap
   size_t team_elems = 0;   // u64 team top-M keys (nq * teams * M) in mc mode
@@ -149,7 +150,7 @@ void launch_team_b1(const float* data, const uint32_t* graph, uint32_t n, uint32
                     uint32_t dim, uint32_t degree, const float* queries, uint32_t nq, uint32_t T,
                     uint32_t M, uint32_t k, uint32_t max_iter, uint32_t min_iter, uint64_t seed,
                     uint64_t query_offset, uint32_t seed_mode, uint32_t* tab, uint32_t hcap,
-                    uint32_t tag, unsigned long long* team_out, void* team_stats,
+                    uint32_t tag, uint32_t direct, unsigned long long* team_out, void* team_stats,
                     uint32_t* done_ctr, uint32_t* out_ids, float* out_dists,
                     uint32_t* out_counts, void* stats, cudaStream_t stream);
 

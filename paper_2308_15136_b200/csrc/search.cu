@@ -644,10 +644,12 @@ search_kernel(const KParams P) {
     S.table = reinterpret_cast<uint32_t*>(p);
   }
   unsigned long long* gtab = SMEM_TABLE ? nullptr : P.gtables + (size_t)blockIdx.x * P.hcap;
-  uint32_t tag = SMEM_TABLE ? 0 : P.gens[blockIdx.x];
+  uint32_t* const bm = P.bitmaps ? P.bitmaps + (size_t)blockIdx.x * P.bm_words : nullptr;
+  // (tags only for the hashed HBM tables: the bitmap and smem tables are
+  // cleared per query)
+  uint32_t tag = SMEM_TABLE || bm ? 0 : P.gens[blockIdx.x];
   const uint32_t mask = P.hcap - 1;
   const bool forget = P.policy == 1;
-  uint32_t* const bm = P.bitmaps ? P.bitmaps + (size_t)blockIdx.x * P.bm_words : nullptr;
 
   for (;;) {
     if (tid == 0) ctl.qi = atomicAdd(P.work, 1u);
@@ -1052,7 +1054,7 @@ search_kernel(const KParams P) {
     }
     __syncthreads();
   }
-  if (!SMEM_TABLE && !P.mc_teams && tid == 0) P.gens[blockIdx.x] = tag;
+  if (!SMEM_TABLE && !bm && !P.mc_teams && tid == 0) P.gens[blockIdx.x] = tag;
 }
 
 // ------------------------------------------------------ K7 team merge ------
@@ -1610,7 +1612,19 @@ SearchPlan plan_search(const DeviceIndexView& ix, const SearchConfig& c, uint32_
   if (pl.mc && team_b1_eligible(c.topm, c.k, T, d, ix.ld)) {
     const char* e = std::getenv("CAGRA_B1_KERNEL");  // "0": the generic multi-CTA kernel
     pl.b1 = !(e && e[0] == '0');
-    if (pl.b1) pl.grid = nq * T;
+    if (pl.b1) {
+      pl.grid = nq * T;
+      // the reference-sized table (hcap slots) as a bitmap of hcap * 32 bits;
+      // when that covers every node id, a bitmap of n bits indexed by id is
+      // smaller and collision-free (the reference's table is exact)
+      const uint32_t nw = round_up_u32((ix.n + 31) / 32, 4);
+      const char* de = std::getenv("CAGRA_B1_DIRECT");  // "0": hashed bits (A/B)
+      if ((uint64_t)pl.hcap * 32 >= ix.n && !(de && de[0] == '0')) {
+        pl.hcap = nw;
+        pl.b1_direct = true;
+      }
+      pl.table_elems = (uint64_t)nq * pl.hcap;  // two regions of nq * hcap words
+    }
   }
   return pl;
 }
@@ -1666,7 +1680,8 @@ uint32_t launch_search(const DeviceIndexView& ix, const SearchConfig& c, const S
     // cleared alternately inside the kernel
     launch_team_b1(ix.data, ix.graph, ix.n, ix.ld, ix.dim, ix.degree, d_queries, nq, pl.teams,
                    c.topm, c.k, pl.max_iter, pl.min_iter, c.seed, c.query_offset, c.seed_mode,
-                   reinterpret_cast<uint32_t*>(d_tables), pl.hcap, mc_tag, d_team_out,
+                   reinterpret_cast<uint32_t*>(d_tables), pl.hcap, mc_tag,
+                   pl.b1_direct ? 1u : 0u, d_team_out,
                    d_team_stats, d_b1_ctr, d_ids, d_dists, d_counts, d_stats, stream);
     return launches;
   }

@@ -55,6 +55,13 @@ namespace {
 
 constexpr int B1_THREADS = 128;
 
+// 1: the visited test is an atomic claim (fetch-OR in flight with the row
+// loads: exact across teams, no separate mark); 0: a plain L2 load of the
+// bitmap word, then a fire-and-forget OR for first visits (racy across teams)
+#ifndef CAGRA_B1_CLAIM
+#define CAGRA_B1_CLAIM 1
+#endif
+
 // Phase profiler (tools/build_variant.sh b1prof -DCAGRA_B1_PROF search_b1):
 // team 0, thread 0 accumulates cycles per phase; printed by the launcher.
 #ifdef CAGRA_B1_PROF
@@ -73,11 +80,21 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+#if !CAGRA_B1_CLAIM
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+#endif
+#if CAGRA_B1_CLAIM
+// atomic OR returning the old word (the visited claim), issued like a load
+__device__ __forceinline__ uint32_t atom_or_u32(uint32_t* p, uint32_t bit) {
+  uint32_t v;
+  asm volatile("atom.global.or.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(bit) : "memory");
+  return v;
+}
+#endif
 __device__ __forceinline__ float4 ldg_f4(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -93,6 +110,7 @@ struct B1Params {
   uint32_t n, ld, dim, degree, T, M, k, max_iter, min_iter;
   uint64_t seed, query_offset;
   uint32_t seed_mode, hcap, tag;
+  uint32_t direct;                 // bit = node id (hcap * 32 >= n), else hash_id
   uint32_t* tab;                   // [2][nq][hcap] u32 words of the visited bitmaps
   unsigned long long* team_out;    // [nq * T][M]
   void* team_stats;                // [nq * T] DevStats-compatible
@@ -313,9 +331,15 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
     const uint32_t my_id =
         sub == 0 ? cid[0]
                  : (sub == 1 ? cid[1] : (sub == 2 ? cid[2] : (sub == 3 ? cid[3] : kInvalidId)));
-    const uint32_t bi = my_id != kInvalidId ? hash_id(my_id, bmask) : 0u;
+    const uint32_t bi = my_id == kInvalidId ? 0u : (P.direct ? my_id : hash_id(my_id, bmask));
     B1_T(p1);
+#if CAGRA_B1_CLAIM
+    // claim: atomic OR returning the old word, in flight with the row loads;
+    // exactly one team wins a node
+    const uint32_t word = my_id != kInvalidId ? atom_or_u32(bits + (bi >> 5), 1u << (bi & 31)) : ~0u;
+#else
     const uint32_t word = ldcg_u32(bits + (bi >> 5));
+#endif
     float4 xv[4][V];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -352,7 +376,9 @@ __global__ void __launch_bounds__(B1_THREADS, 1) team_b1_kernel(const B1Params P
     // first visit = bit clear; mark it (fire-and-forget atomic OR, never
     // waited on: the barrier below orders it for this team's next tests)
     const bool mine_first = my_id != kInvalidId && !((word >> (bi & 31)) & 1u) && sub < 4;
+#if !CAGRA_B1_CLAIM
     if (mine_first) atomicOr(bits + (bi >> 5), 1u << (bi & 31));
+#endif
     const unsigned fb = __ballot_sync(0xffffffffu, mine_first);
     const uint32_t firstm = (fb >> (lane & ~7)) & 0xfu;
     // survivors: candidate c's fixed slot holds its key, or a dummy (the
@@ -509,7 +535,7 @@ void launch_team_b1(const float* data, const uint32_t* graph, uint32_t n, uint32
                     uint32_t dim, uint32_t degree, const float* queries, uint32_t nq, uint32_t T,
                     uint32_t M, uint32_t k, uint32_t max_iter, uint32_t min_iter, uint64_t seed,
                     uint64_t query_offset, uint32_t seed_mode, uint32_t* tab, uint32_t hcap,
-                    uint32_t tag, unsigned long long* team_out, void* team_stats,
+                    uint32_t tag, uint32_t direct, unsigned long long* team_out, void* team_stats,
                     uint32_t* done_ctr, uint32_t* out_ids, float* out_dists,
                     uint32_t* out_counts, void* stats, cudaStream_t stream) {
   B1Params P;
@@ -530,6 +556,7 @@ void launch_team_b1(const float* data, const uint32_t* graph, uint32_t n, uint32
   P.seed_mode = seed_mode;
   P.hcap = hcap;
   P.tag = tag;
+  P.direct = direct;
   P.tab = tab;
   P.team_out = team_out;
   P.team_stats = team_stats;
