@@ -60,25 +60,46 @@ __device__ void block_bitonic_sort(uint64_t* a, uint32_t P) {
 }
 
 // ------------------------------------------------------------------- K2 ---
-// Shared layout: xrow[deg] | hkey[H] | hrank[H] | counts[deg] | keys[P] (u64)
+// rank_of(X) as an open-addressing table of packed (rank << 32 | id) slots,
+// sized 8 deg (load <= 1/8: a miss — most probes, since most two-hop ids are
+// not in X's row — costs about one 8-byte shared load), indexed by the high
+// bits of a multiplicative hash.
+constexpr uint64_t kSlotEmpty = ~0ull;
+
+__device__ __forceinline__ uint32_t slot_of(uint32_t id, uint32_t hshift) {
+  return (id * 2654435761u) >> hshift;
+}
+
+__device__ __forceinline__ uint32_t rank_lookup(const uint64_t* tab, uint32_t hmask,
+                                                uint32_t hshift, uint32_t y) {
+  uint32_t h = slot_of(y, hshift);
+  for (;;) {
+    const uint64_t e = tab[h];
+    if (static_cast<uint32_t>(e) == y) return static_cast<uint32_t>(e >> 32);
+    if (e == kSlotEmpty) return kInvalidId;
+    h = (h + 1) & hmask;
+  }
+}
+
+// Shared layout: tab[H] (u64, 16-byte aligned) | keys[P] (u64) | xrow[deg] | counts[deg]
 __global__ void __launch_bounds__(OPT_NT)
 detour_reorder_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t deg, uint32_t d,
                       uint32_t H, uint32_t P, const uint32_t* __restrict__ counts_in,
                       uint32_t* __restrict__ counts_out, uint32_t* __restrict__ pruned_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* keys = tab + H;
   uint32_t* xrow = reinterpret_cast<uint32_t*>(keys + P);
-  uint32_t* hkey = xrow + deg;
-  uint32_t* hrank = hkey + H;
-  uint32_t* counts = hrank + H;
-  const uint32_t hmask = H - 1;
+  uint32_t* counts = xrow + deg;
+  const uint32_t hmask = H - 1, hshift = 32u - __ffs(H) + 1u;  // H = 2^b: shift 32 - b
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
   for (uint32_t x = blockIdx.x; x < n; x += gridDim.x) {
     const uint32_t* xr = knn + (size_t)x * deg;
-    for (uint32_t i = tid; i < H; i += blockDim.x) {
-      hkey[i] = kInvalidId;
-      hrank[i] = kInvalidId;
+    if (counts_in == nullptr) {
+      uint4* t4 = reinterpret_cast<uint4*>(tab);  // H >= 2: whole 16-byte pairs
+      for (uint32_t i = tid; i < H / 2; i += blockDim.x)
+        t4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
     for (uint32_t r = tid; r < deg; r += blockDim.x) {
       xrow[r] = xr[r];
@@ -86,40 +107,66 @@ detour_reorder_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t deg
     }
     __syncthreads();
     if (counts_in == nullptr) {
-      // rank_of: first occurrence wins (unordered_map::emplace, graph_opt.cpp:62)
+      // rank_of: first occurrence wins (unordered_map::emplace, graph_opt.cpp:62):
+      // a repeated id keeps the smaller rank (same low word -> u64 min)
       for (uint32_t r = tid; r < deg; r += blockDim.x) {
-        uint32_t id = xrow[r];
-        uint32_t h = hash_id(id, hmask);
+        const uint32_t id = xrow[r];
+        const uint64_t e = ((uint64_t)r << 32) | id;
+        uint32_t h = slot_of(id, hshift);
         for (;;) {
-          uint32_t old = atomicCAS(&hkey[h], kInvalidId, id);
-          if (old == kInvalidId || old == id) break;
+          const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long*>(&tab[h]),
+                                         kSlotEmpty, e);
+          if (old == kSlotEmpty) break;
+          if (static_cast<uint32_t>(old) == id) {
+            atomicMin(reinterpret_cast<unsigned long long*>(&tab[h]), e);
+            break;
+          }
           h = (h + 1) & hmask;
         }
-        atomicMin(&hrank[h], r);
       }
       __syncthreads();
       // X -> Z (rank rz) -> Y (rank rzy in Z's row); X -> Y at rank ry.
       // Only routes with max(rz, rzy) < ry count (graph_opt.cpp:74-93), so
-      // rz and rzy never need to reach deg-1.
-      for (uint32_t rz = warp; rz + 1 < deg; rz += nwarps) {
-        const uint32_t* zr = knn + (size_t)xrow[rz] * deg;
-        for (uint32_t rzy = lane; rzy + 1 < deg; rzy += 32) {
-          uint32_t y = __ldg(&zr[rzy]);
-          if (y == x) continue;
-          uint32_t h = hash_id(y, hmask);
-          uint32_t ry = kInvalidId;
-          for (;;) {
-            uint32_t k = hkey[h];
-            if (k == y) {
-              ry = hrank[h];
-              break;
-            }
-            if (k == kInvalidId) break;
-            h = (h + 1) & hmask;
+      // rz and rzy never need to reach deg-1.  The counts are integer sums:
+      // the order of the additions does not matter.
+      const uint32_t last = deg - 1;
+      if ((deg & 3) == 0 && deg <= 128) {
+        // Z rows as one 16-byte load per lane (lane l: ranks 4l..4l+3), R rows
+        // per warp in flight together
+        constexpr uint32_t R = 4;
+        for (uint32_t rz0 = warp * R; rz0 < last; rz0 += nwarps * R) {
+          uint4 v[R];
+#pragma unroll
+          for (uint32_t u = 0; u < R; ++u) {
+            const uint32_t rz = rz0 + u;
+            v[u] = rz < last && lane * 4 < deg
+                       ? __ldg(reinterpret_cast<const uint4*>(knn + (size_t)xrow[rz] * deg) + lane)
+                       : make_uint4(x, x, x, x);  // y == x: skipped
           }
-          if (ry == kInvalidId || ry == rz) continue;
-          uint32_t mx = rz > rzy ? rz : rzy;
-          if (mx < ry) atomicAdd(&counts[ry], 1u);
+#pragma unroll
+          for (uint32_t u = 0; u < R; ++u) {
+            const uint32_t rz = rz0 + u;
+            const uint32_t ys[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (uint32_t e = 0; e < 4; ++e) {
+              const uint32_t rzy = lane * 4 + e, y = ys[e];
+              if (rzy >= last || y == x) continue;
+              const uint32_t ry = rank_lookup(tab, hmask, hshift, y);
+              if (ry == kInvalidId || ry == rz) continue;
+              if ((rz > rzy ? rz : rzy) < ry) atomicAdd(&counts[ry], 1u);
+            }
+          }
+        }
+      } else {
+        for (uint32_t rz = warp; rz < last; rz += nwarps) {
+          const uint32_t* zr = knn + (size_t)xrow[rz] * deg;
+          for (uint32_t rzy = lane; rzy < last; rzy += 32) {
+            const uint32_t y = __ldg(&zr[rzy]);
+            if (y == x) continue;
+            const uint32_t ry = rank_lookup(tab, hmask, hshift, y);
+            if (ry == kInvalidId || ry == rz) continue;
+            if ((rz > rzy ? rz : rzy) < ry) atomicAdd(&counts[ry], 1u);
+          }
         }
       }
       __syncthreads();
@@ -215,7 +262,7 @@ detour_distance_kernel(const uint32_t* __restrict__ knn, uint32_t n, uint32_t de
 }
 
 size_t detour_smem(uint32_t deg, uint32_t H, uint32_t P) {
-  return sizeof(uint64_t) * P + sizeof(uint32_t) * (deg + 2 * H + deg);
+  return sizeof(uint64_t) * (P + H) + sizeof(uint32_t) * 2 * deg;
 }
 
 // ------------------------------------------------------------------- K3 ---
@@ -456,8 +503,9 @@ void launch_check_ids(const uint32_t* d_ids, uint64_t count, uint32_t n, int* d_
 static void detour_launch(const uint32_t* d_knn, const uint32_t* d_counts_in, uint32_t n,
                           uint32_t deg, uint32_t d, uint32_t* d_counts_out,
                           uint32_t* d_pruned_out, cudaStream_t stream) {
-  uint32_t H = next_pow2_u32(2 * deg);
+  uint32_t H = next_pow2_u32(8 * deg);  // load <= 1/8 (rank_lookup)
   uint32_t P = next_pow2_u32(deg);
+  while (H > 2 * P && detour_smem(deg, H, P) > 48 * 1024) H >>= 1;  // keep 4+ CTAs per SM
   size_t smem = detour_smem(deg, H, P);
   if (smem > 200 * 1024) throw UsageErr("optimize: input degree too large for the device kernel");
   CAGRA_CUDA_TRY(cudaFuncSetAttribute(detour_reorder_kernel,
