@@ -167,6 +167,36 @@ __device__ __forceinline__ float seq_dist(const float* __restrict__ x, const flo
   for (; i < dim; ++i) acc = seq_step(acc, __ldg(x + i), __ldg(q + i));
   return acc;
 }
+// U independent sequential chains (U rows against one query) interleaved:
+// U x the arithmetic ILP and U x the loads in flight of seq_dist; each chain
+// keeps index order, so every result is bit-equal to seq_dist.
+template <int U>
+__device__ __forceinline__ void seq_dist_multi(const float* const (&x)[U],
+                                               const float* __restrict__ q, uint32_t dim,
+                                               float (&acc)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0f;
+  uint32_t i = 0;
+#pragma unroll 2
+  for (; i + 4 <= dim; i += 4) {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(q + i));
+    float4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = __ldg(reinterpret_cast<const float4*>(x[u] + i));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[u] = seq_step(acc[u], a[u].x, b.x);
+      acc[u] = seq_step(acc[u], a[u].y, b.y);
+      acc[u] = seq_step(acc[u], a[u].z, b.z);
+      acc[u] = seq_step(acc[u], a[u].w, b.w);
+    }
+  }
+  for (; i < dim; ++i) {
+    const float b = __ldg(q + i);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = seq_step(acc[u], __ldg(x[u] + i), b);
+  }
+}
 #endif
 
 // ---- host-side error types; capi.cu maps them to status codes ----

@@ -961,64 +961,100 @@ __device__ __forceinline__ void sort_keys_inplace(uint64_t* b, uint32_t c, int l
 // d~ <= tau* (tau* from the sample pass).  Valid iff K <= count <= capg and
 // d~_(K) + 2 delta <= tau* (then every point that can be a true top-K member
 // is in the buffer); otherwise the row is queued for the list-mode pass.
-__global__ void tc_rerank_append_kernel(uint64_t* __restrict__ bufs,
-                                        const uint32_t* __restrict__ bcount, uint32_t capg,
-                                        const uint64_t* __restrict__ tau_keys, uint32_t tau_ld,
-                                        uint32_t nq, uint32_t K, const float* __restrict__ qnorm,
-                                        float xm, float dscale, float eps_rel,
-                                        float eps_norm, const float* __restrict__ data, uint32_t ld,
-                                        const float* __restrict__ queries, uint32_t qld,
-                                        uint32_t dim, uint32_t* __restrict__ out_ids,
-                                        float* __restrict__ out_dists,
-                                        uint32_t* __restrict__ fail_rows,
-                                        uint32_t* __restrict__ fail_cnt,
-                                        unsigned long long* __restrict__ reranked) {
-  const uint32_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= nq) return;
-  const uint32_t c = bcount[row];
-  const float tau_star = key_dist(tau_keys[(size_t)row * tau_ld + tau_ld - 1]);
+// Two instantiations keep the common case light on registers (occupancy is
+// what hides the row gathers): ES = 16 sorts rows of <= 512 keys and queues
+// larger ones on `big`; ES = 32 then runs over the `big` rows only.
+struct AppendRerank {
+  uint64_t* bufs;
+  const uint32_t* bcount;
+  uint32_t capg;
+  const uint64_t* tau_keys;
+  uint32_t tau_ld, nq, K;
+  const float* qnorm;
+  float xm, dscale, eps_rel, eps_norm;
+  const float* data;
+  uint32_t ld;
+  const float* queries;
+  uint32_t qld, dim;
+  uint32_t* out_ids;
+  float* out_dists;
+  uint32_t* fail_rows;
+  uint32_t* fail_cnt;
+  uint32_t* big_rows;  // [0] = count, rows from [1]
+  unsigned long long* reranked;
+};
+
+template <int ES>
+__device__ __forceinline__ void rerank_append_row(const AppendRerank& A, uint32_t row, int lane) {
+  uint64_t* __restrict__ bufs = A.bufs;
+  const uint32_t capg = A.capg, K = A.K, ld = A.ld, qld = A.qld, dim = A.dim;
+  const float xm = A.xm, dscale = A.dscale, eps_rel = A.eps_rel, eps_norm = A.eps_norm;
+  const float* __restrict__ data = A.data;
+  const float* __restrict__ queries = A.queries;
+  const uint32_t c = A.bcount[row];
+  const float tau_star = key_dist(A.tau_keys[(size_t)row * A.tau_ld + A.tau_ld - 1]);
   uint64_t* b = bufs + (size_t)row * capg;
   bool ok = c >= K && c <= capg;
   float bound = 0.0f;
   if (ok) {
     // the smallest warp sort that holds the row's keys (typically ~430)
-    if (c <= 256) sort_keys_inplace<8>(b, c, lane);
-    else if (c <= 512) sort_keys_inplace<16>(b, c, lane);
-    else sort_keys_inplace<32>(b, c, lane);
-    const float qn = qnorm[row];
+    if (c <= 256) {
+      sort_keys_inplace<8>(b, c, lane);
+    } else if (c <= 512) {
+      sort_keys_inplace<16>(b, c, lane);
+    } else if (ES == 32) {
+      sort_keys_inplace<32>(b, c, lane);
+    } else {
+      if (lane == 0) A.big_rows[1 + atomicAdd(A.big_rows, 1u)] = row;
+      return;
+    }
+    const float qn = A.qnorm[row];
     const float delta = eps_rel * sqrtf(qn) * sqrtf(xm) + eps_norm * (qn + xm);
     bound = key_dist(b[K - 1]) + 2.0f * delta * dscale;
     ok = bound <= tau_star;
   }
   if (!ok) {
-    if (lane == 0) fail_rows[atomicAdd(fail_cnt, 1u)] = row;
+    if (lane == 0) A.fail_rows[atomicAdd(A.fail_cnt, 1u)] = row;
     return;
   }
-  // exact sequential-chain distances for the band, cyclic over lanes
-  constexpr int E2 = 8;
+  // exact sequential-chain distances for the band, cyclic over lanes: slot
+  // e * 32 + lane of the sorted buffer; 4 slots' chains interleaved, and a
+  // group is skipped once no lane's slot is in the band (the buffer is sorted)
+  constexpr int E2 = 8, G = 4;
   uint64_t w[E2];
   const float* q = queries + (size_t)row * qld;
   uint32_t nre = 0;
   bool over = false;
 #pragma unroll
-  for (int e = 0; e < E2; ++e) {
-    const uint32_t i = e * 32 + lane;
-    uint64_t key = i < c ? b[i] : kDummyKey;
-    if (!key_is_dummy(key) && key_dist(key) <= bound) {
-      const uint32_t id = key_id(key);
-      const float* x = data + (size_t)id * ld;
-      const float acc = seq_dist(x, q, dim);
-      w[e] = make_key(acc, id);
-      ++nre;
-    } else {
-      w[e] = kDummyKey;
+  for (int e0 = 0; e0 < E2; e0 += G) {
+    uint32_t id[G];
+    bool in[G];
+    const float* xs[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const uint32_t i = (e0 + u) * 32 + lane;
+      const uint64_t key = i < c ? b[i] : kDummyKey;
+      in[u] = !key_is_dummy(key) && key_dist(key) <= bound;
+      id[u] = in[u] ? key_id(key) : key_id(b[0]);  // out of band: a cached row
+      xs[u] = data + (size_t)id[u] * ld;
+    }
+    if (!__any_sync(0xffffffffu, in[0])) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) w[e0 + u] = kDummyKey;
+      continue;
+    }
+    float acc[G];
+    seq_dist_multi<G>(xs, q, dim, acc);
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      w[e0 + u] = in[u] ? make_key(acc[u], id[u]) : kDummyKey;
+      nre += in[u] ? 1u : 0u;
     }
   }
   // the band must fit the 256 re-rank slots
   if (c > 32 * E2 && key_dist(b[32 * E2]) <= bound) over = true;
   if (__any_sync(0xffffffffu, over)) {
-    if (lane == 0) fail_rows[atomicAdd(fail_cnt, 1u)] = row;
+    if (lane == 0) A.fail_rows[atomicAdd(A.fail_cnt, 1u)] = row;
     return;
   }
   warp_sort_regs<E2>(w, lane);
@@ -1026,13 +1062,27 @@ __global__ void tc_rerank_append_kernel(uint64_t* __restrict__ bufs,
   for (int e = 0; e < E2; ++e) {
     const uint32_t i = lane * E2 + e;
     if (i < K) {
-      out_ids[(size_t)row * K + i] = key_id(w[e]);
-      out_dists[(size_t)row * K + i] = key_dist(w[e]);
+      A.out_ids[(size_t)row * K + i] = key_id(w[e]);
+      A.out_dists[(size_t)row * K + i] = key_dist(w[e]);
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nre += __shfl_xor_sync(0xffffffffu, nre, o);
-  if (lane == 0 && reranked) atomicAdd(reranked, (unsigned long long)nre);
+  if (lane == 0 && A.reranked) atomicAdd(A.reranked, (unsigned long long)nre);
+}
+
+// ES = 16: every row (grid covers nq warps); ES = 32: the queued big rows
+template <int ES>
+__global__ void __launch_bounds__(256, ES == 16 ? 3 : 1) tc_rerank_append_kernel(const AppendRerank A) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (ES == 16) {
+    if (w < A.nq) rerank_append_row<16>(A, w, lane);
+  } else {
+    const uint32_t nb = *(volatile const uint32_t*)A.big_rows;
+    for (uint32_t i = w; i < nb; i += gridDim.x * (blockDim.x / 32))
+      rerank_append_row<32>(A, A.big_rows[1 + i], lane);
+  }
 }
 
 // Column-split list passes: per row, merge groups of up to m sorted KC-key
@@ -1659,7 +1709,7 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     const uint32_t capg = 1024;
     const uint32_t cmax = std::min(nq, kChunk);
     View lists1{arena(kSlotLists, 8ull * r * cmax)}, bufs{arena(kSlotBufs, 8ull * cmax * capg)},
-        bcount{arena(kSlotBcount, 4ull * cmax)}, fails{arena(kSlotFails, 4ull * cmax + 4)},
+        bcount{arena(kSlotBcount, 4ull * cmax)}, fails{arena(kSlotFails, 8ull * cmax + 8)},
         rer{arena(kSlotRer, 8)};
     const uint32_t brows = BOX_ROWS;  // every B load is one or more 64-point boxes
     const bool f16 = c.terms == 1;
@@ -1674,7 +1724,8 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       float* cdists = d_dists + (size_t)q0 * K;
       TcCall cc = c;
       cc.self_base = c.self_base + q0;
-      CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4ull * cq + 4, stream));
+      CAGRA_CUDA_TRY(cudaMemsetAsync(fails.p, 0, 4, stream));  // the fail count
+      CAGRA_CUDA_TRY(cudaMemsetAsync(fails.as<uint32_t>() + 1 + cmax, 0, 4, stream));  // big count
       CAGRA_CUDA_TRY(cudaMemsetAsync(rer.p, 0, 8, stream));
       CAGRA_CUDA_TRY(cudaMemsetAsync(bcount.p, 0, 4ull * cq, stream));  // append counters
       CUtensorMap tmA = make_map(Pq, cq, c.Kp, 1, TC_BN, f16);
@@ -1708,10 +1759,32 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
       tr.mark("full");
       uint32_t* fail_cnt = fails.as<uint32_t>();
       uint32_t* fail_rows = fail_cnt + 1;
-      tc_rerank_append_kernel<<<(cq + 7) / 8, 256, 0, stream>>>(
-          bufs.as<uint64_t>(), bcount.as<uint32_t>(), capg, lists1.as<uint64_t>(), r, cq, K,
-          qnorm, c.xm, c.dscale, c.eps_rel, c.eps_norm, d_data, ld, cqueries, qld, dim, cids,
-          cdists, fail_rows, fail_cnt, rer.as<unsigned long long>());
+      AppendRerank ar;
+      ar.bufs = bufs.as<uint64_t>();
+      ar.bcount = bcount.as<uint32_t>();
+      ar.capg = capg;
+      ar.tau_keys = lists1.as<uint64_t>();
+      ar.tau_ld = r;
+      ar.nq = cq;
+      ar.K = K;
+      ar.qnorm = qnorm;
+      ar.xm = c.xm;
+      ar.dscale = c.dscale;
+      ar.eps_rel = c.eps_rel;
+      ar.eps_norm = c.eps_norm;
+      ar.data = d_data;
+      ar.ld = ld;
+      ar.queries = cqueries;
+      ar.qld = qld;
+      ar.dim = dim;
+      ar.out_ids = cids;
+      ar.out_dists = cdists;
+      ar.fail_rows = fail_rows;
+      ar.fail_cnt = fail_cnt;
+      ar.big_rows = fail_rows + cmax;  // [count, rows...] after the fail list
+      ar.reranked = rer.as<unsigned long long>();
+      tc_rerank_append_kernel<16><<<(cq + 7) / 8, 256, 0, stream>>>(ar);
+      tc_rerank_append_kernel<32><<<std::min<uint32_t>((cq + 7) / 8, 148 * 8), 256, 0, stream>>>(ar);
       CAGRA_LAUNCH_CHECK();
       uint32_t nf = 0;
       unsigned long long nre = 0;
