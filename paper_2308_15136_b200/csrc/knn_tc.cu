@@ -86,6 +86,10 @@ constexpr uint32_t BOX_BYTES = BOX_ROWS * TC_BK * 2;  // 8 KB
 // epilogue instead of 1 (the epilogue's per-tile latency varies with its
 // appends). Measured slower on 1M x 96 k=128 (0.60 s vs 0.404 s: twice the
 // per-tile barrier and release work), so 128-point tiles stay the default.
+// 1: mode-2 lists kept unsorted with a tracked maximum (see drain)
+#ifndef CAGRA_TC_MAXLIST
+#define CAGRA_TC_MAXLIST 1
+#endif
 #ifndef CAGRA_TC_W64
 #define CAGRA_TC_W64 0
 #endif
@@ -313,10 +317,12 @@ __device__ __forceinline__ float chunk_min(const uint32_t (&v)[32], float (&m3)[
 // own TMEM accumulators, and 8 epilogue warps (two per TMEM lane quarter)
 // scan them — twice the epilogue issue slots per SM and half the L2->SM B
 // traffic per query row of HV = 1.
-template <bool PAIR, bool SA = false, int HV = 1>
+template <bool PAIR, bool SA = false, int HV = 1, int MODE = -1>
 __global__ void __launch_bounds__(64 + 128 * HV, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const TcArgs P) {
+  // MODE >= 0: the epilogue mode fixed at compile time (no dead mode code)
+  const uint32_t kmode = MODE >= 0 ? (uint32_t)MODE : P.mode;
   static_assert(!(PAIR && SA), "streamed A is single-CTA");
   static_assert(HV == 1 || (!PAIR && !SA), "two halves: single CTA, resident A");
   constexpr bool TS = CAGRA_KNN_TS && !PAIR && !SA && HV == 1;
@@ -510,19 +516,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       __syncwarp();
       if (lane == 0) mbar_arrive(afull);
     }
-    if (P.mode == 0) {
+    if (kmode == 0) {
       for (uint32_t r = 0; r < 32; ++r) {          // lists start as dummies (coalesced)
         const uint32_t rr = row0 + hv * TC_BM + q4 * 32 + r;
         if (rr < P.nq)
           for (uint32_t i = lane; i < P.KC; i += 32) lists[(size_t)rr * P.KC + i] = kDummyKey;
       }
     }
-    if (P.mode == 2)  // the row's list starts as dummies
+    if (kmode == 2)  // the row's list starts as dummies
       for (uint32_t i = 0; i < P.KC; ++i) mypend[i * ROWS + rl] = kDummyKey;
     __syncwarp();
     uint64_t tau = kDummyKey;
     float tau_f = __int_as_float(0x7f800000);
-    if (P.mode == 1 && live)
+    if (kmode == 1 && live)
       tau_f = key_dist(P.tau_keys[(size_t)row * P.tau_ld + P.tau_ld - 1]);
     // FP16 split: the GEMM yields e = s^2 (|x'|^2 - 2 q'.x'); the row constant
     // qoff = s^2 |q'|^2 completes d~ = e + qoff.  The chunk test compares e
@@ -610,7 +616,37 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     // mode 2: the row's sorted list occupies pending slots [0, KC); new keys
     // are appended behind it and drained into it by per-lane insertion
     // (thread = row, no warp cooperation; the threshold is the list's last key)
-    const uint32_t pbase = P.mode == 2 ? P.KC : 0u;
+    const uint32_t pbase = kmode == 2 ? P.KC : 0u;
+#if CAGRA_TC_MAXLIST
+    // mode 2 as an UNSORTED list of KC keys whose maximum (the threshold) sits
+    // at slot tmax: a key below it replaces it, then the maximum is found
+    // again with KC independent shared loads (no dependent shift chain).  The
+    // consumers read only the maximum (at KC - 1, placed after the pass) or
+    // sort the list themselves.
+    uint32_t tmax = 0;
+    auto drain = [&]() {
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint64_t key = mypend[(pbase + i) * ROWS + rl];
+        if (key >= tau) continue;
+        mypend[tmax * ROWS + rl] = key;
+        uint64_t m = 0;
+        uint32_t mi = 0;
+#pragma unroll 8
+        for (uint32_t j = 0; j < P.KC; ++j) {
+          const uint64_t v = mypend[j * ROWS + rl];
+          if (v > m) {
+            m = v;
+            mi = j;
+          }
+        }
+        tau = m;
+        tmax = mi;
+      }
+      cnt = 0;
+      tau_f = key_dist(tau);
+      tau_e = tau_e_of(tau_f);
+    };
+#else
     auto drain = [&]() {
       for (uint32_t i = 0; i < cnt; ++i) {
         const uint64_t key = mypend[(pbase + i) * ROWS + rl];
@@ -628,9 +664,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tau_f = key_dist(tau);
       tau_e = tau_e_of(tau_f);
     };
+#endif
 #if !CAGRA_TC_STAGED_APPEND
     // append mode: each lane owns its row's global buffer (no staging)
-    uint64_t* const row_buf = P.mode == 1 && live ? P.bufs + (size_t)row * P.capg : nullptr;
+    uint64_t* const row_buf = kmode == 1 && live ? P.bufs + (size_t)row * P.capg : nullptr;
 #endif
     // slow path of one 32-column chunk: only the FMNMX3 groups whose minimum
     // passes are examined element by element (appends are rare after the
@@ -643,7 +680,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (d <= tau_f && col < P.n && col != self_c) {
             const uint64_t key = make_key(fmaxf(d, 0.0f), col * P.col_stride);
 #if !CAGRA_TC_STAGED_APPEND
-            if (P.mode == 1) {  // straight into the row's global buffer
+            if (kmode == 1) {  // straight into the row's global buffer
               if (gcnt < P.capg) row_buf[gcnt] = key;
               ++gcnt;
               return;
@@ -666,11 +703,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           take(31);
         }
       }
-      if (P.mode == 2) {
+      if (kmode == 2) {
         if (cnt) drain();
-      } else if ((!(CAGRA_TC_STAGED_APPEND == 0) || P.mode == 0) &&
+      } else if ((!(CAGRA_TC_STAGED_APPEND == 0) || kmode == 0) &&
                  __any_sync(0xffffffffu, cnt > P.pend_cap - 32)) {
-        if (P.mode == 0) flush(TC_PEND / 4);
+        if (kmode == 0) flush(TC_PEND / 4);
         else spill();
       }
     };
@@ -706,9 +743,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         scan(vb, mb, cbase + 32, hitb);
       }
     }
-    if (P.mode == 0) {
+    if (kmode == 0) {
       flush(0);
-    } else if (P.mode == 2) {
+    } else if (kmode == 2) {
+#if CAGRA_TC_MAXLIST
+      if (live && tmax != P.KC - 1) {  // the maximum goes last
+        const uint64_t a = mypend[tmax * ROWS + rl];
+        mypend[tmax * ROWS + rl] = mypend[(P.KC - 1) * ROWS + rl];
+        mypend[(P.KC - 1) * ROWS + rl] = a;
+      }
+#endif
       if (live)
         for (uint32_t i = 0; i < P.KC; ++i)
           lists[(size_t)row * P.KC + i] = mypend[i * ROWS + rl];
@@ -1406,11 +1450,14 @@ void run_tc_kernel(const TcCall& c, const void* Pq, const CUtensorMap& tmA,
   a.nq = nq;
   const size_t smem = tc_smem_bytes(c.kblocks, a.stages, a.pend_cap, pair, hv);
   if (!sa && !pair && hv == 2) {
-    CAGRA_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<false, false, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    knn_tc_kernel<false, false, 2>
-        <<<dim3((nq + 2 * TC_BM - 1) / (2 * TC_BM), splits), 64 + 2 * TC_BM, smem, c.stream>>>(
-            tmA, tmB, a);
+    // one instantiation per epilogue mode: the hot full pass carries no
+    // list/insertion code (registers and code size)
+    auto fn = a.mode == 1 ? knn_tc_kernel<false, false, 2, 1>
+                          : (a.mode == 2 ? knn_tc_kernel<false, false, 2, 2>
+                                         : knn_tc_kernel<false, false, 2, 0>);
+    CAGRA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<dim3((nq + 2 * TC_BM - 1) / (2 * TC_BM), splits), 64 + 2 * TC_BM, smem, c.stream>>>(
+        tmA, tmB, a);
     CAGRA_LAUNCH_CHECK();
     return;
   }
