@@ -1460,6 +1460,9 @@ using KernelFn = void (*)(const KParams);
 
 // multi-CTA mode (fast distances only): speculative-insert instantiation
 KernelFn mc_fn(Variant v) {
+#ifdef CAGRA_AB_HOT_ONLY  // A/B libraries: only the 96-d kernels (ptxas in ~1 min)
+  return search_kernel<8, 3, false, false, true>;
+#else
   switch (v.team * 100 + v.maxc) {
     case 402: return search_kernel<4, 2, false, false, true>;
     case 803: return search_kernel<8, 3, false, false, true>;
@@ -1468,11 +1471,15 @@ KernelFn mc_fn(Variant v) {
     case 3208: return search_kernel<32, 8, false, false, true>;
     default: return search_kernel<32, 0, false, false>;
   }
+#endif
 }
 
 template <bool EXACT, bool SMEM>
 KernelFn per_query_fn(Variant v) {
   if (EXACT) return search_kernel<32, 1, true, SMEM>;
+#ifdef CAGRA_AB_HOT_ONLY
+  return search_kernel<8, 3, false, SMEM>;
+#else
   switch (v.team * 100 + v.maxc) {
     case 402: return search_kernel<4, 2, false, SMEM>;
     case 803: return search_kernel<8, 3, false, SMEM>;
@@ -1481,10 +1488,14 @@ KernelFn per_query_fn(Variant v) {
     case 3208: return search_kernel<32, 8, false, SMEM>;
     default: return search_kernel<32, 0, false, SMEM>;
   }
+#endif
 }
 
 KernelFn shared_fn(bool exact, Variant v) {
   if (exact) return shared_search_kernel<32, 1, true>;
+#ifdef CAGRA_AB_HOT_ONLY
+  return shared_search_kernel<8, 3, false>;
+#else
   switch (v.team * 100 + v.maxc) {
     case 402: return shared_search_kernel<4, 2, false>;
     case 803: return shared_search_kernel<8, 3, false>;
@@ -1493,6 +1504,7 @@ KernelFn shared_fn(bool exact, Variant v) {
     case 3208: return shared_search_kernel<32, 8, false>;
     default: return shared_search_kernel<32, 0, false>;
   }
+#endif
 }
 
 }  // namespace
