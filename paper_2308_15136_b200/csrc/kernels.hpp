@@ -125,6 +125,7 @@ struct SearchPlan {
   bool b1 = false;         // mc via the fused small-team kernel (search_b1.cu)
   bool b1_direct = false;  // its visited bitmap indexed by node id (hcap words >= n bits)
   bool bitmap = false;     // standard policy: exact visited bitmap per resident CTA
+  bool inplace = false;    // per-query kernel: one top-M buffer (update_topm in place)
   uint32_t bm_words = 0;   // u32 words per CTA bitmap
   size_t team_elems = 0;   // u64 team top-M keys (nq * teams * M) in mc mode
   const void* fn = nullptr;

@@ -530,7 +530,12 @@ def test_search_empty_batch_and_limits(gpu, oracle):
     assert ids.shape == (0, 10) and counts.shape == (0,)
     # parameters beyond the device's shared-memory budget fail loudly (UsageError)
     with pytest.raises(fodg.UsageError):
-        ix.search(data[:2], fodg.SearchParams(k=10, topm=20000, width=64))
+        ix.search(data[:2], fodg.SearchParams(k=10, topm=30000, width=64))
+    # M = 20000 fits with the in-place top-M update (one 160 KB list) and
+    # returns the exact top-10 (M exceeds n: every node gets evaluated)
+    ids, dists, counts, _ = ix.search(data[:2], fodg.SearchParams(k=10, topm=20000, width=64))
+    gt, _ = fodg.exact_topk_batch(ds, data[:2], 10)
+    assert (counts == 10).all() and np.array_equal(np.sort(ids, 1), np.sort(gt, 1))
     # dimension mismatch / graph-dataset mismatch, reference messages' classes
     with pytest.raises(fodg.UsageError):
         fodg.batch_search(g, ds, fodg.Dataset.from_array(data[:3, :4]), fodg.SearchParams())
