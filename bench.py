@@ -680,11 +680,18 @@ def run_query_sharded(args, D):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "search_kernel (single-CTA beam search)",
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         # the access pattern's own ceiling: random whole-row
+                         # gathers with nothing else in the loop (committed
+                         # measurement, profiles/r02_gather_ceiling.txt)
+                         "gather_ceiling": gather_ceiling(args.n, args.dim)},
             "clocks": clocks,
             "gpu_launches": launches,
             "cpu_baseline": cpu,
         }
+        gc = line["roofline"]["gather_ceiling"]
+        if gc:
+            gc["frac"] = achieved / gc["gbs"]
         if parity is not None:
             line["parity"] = parity
         if cpu and cpu.get("mean_distance_evals") and args.cpu_hash == "standard" and \
@@ -745,6 +752,17 @@ def cpu_batch_legs(args, data, graph, queries, gt, gpu_ids):
            "sample": f"first {sample} of the {args.batch} batch queries, same index, "
                      f"fodg::batch_search per-query mode, {threads} threads"}
     return cpu, parity
+
+
+def gather_ceiling(n, dim):
+    """Measured random-row-gather ceiling (tools/cpp/gather_peak.cu on one B200,
+    best of 1-6 rows in flight per 8-lane team, 4 CTAs/SM) for 384-byte rows:
+    8861 GB/s at 1M rows (L2 reuse included), 6961 at 10M, 6824 at 40M.
+    None for other row sizes."""
+    if dim != 96:
+        return None
+    gbs = 8861.0 if n <= 2_000_000 else (6961.0 if n <= 20_000_000 else 6824.0)
+    return {"gbs": gbs, "source": "profiles/r02_gather_ceiling.txt (tools/cpp/gather_peak.cu)"}
 
 
 def cpu_batch1_legs(args, data, graph, queries, gt, gpu_b1_ids):
