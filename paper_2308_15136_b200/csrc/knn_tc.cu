@@ -1751,8 +1751,10 @@ void launch_knn_tc(const float* d_data, uint32_t n, uint32_t ld, const float* d_
     // r-th smallest of the sample: ~16 r points per row pass tau* (>= K plus
     // the band with margin: 16 x 24 = 384, standard deviation ~80); r <= 24
     // keeps the sample pass's smem lists next to two A halves
-    const uint32_t r = std::min<uint32_t>(
+    uint32_t r = std::min<uint32_t>(
         24, std::max<uint32_t>(8, (3 * (K + 16) + kSampleStride - 1) / kSampleStride));
+    if (const char* er = std::getenv("CAGRA_TC_SAMPLE_R"))  // A/B: sample rank (8..24)
+      r = std::min<uint32_t>(24, std::max<uint32_t>(8, (uint32_t)std::atoi(er)));
     const uint32_t capg = 1024;
     const uint32_t cmax = std::min(nq, kChunk);
     View lists1{arena(kSlotLists, 8ull * r * cmax)}, bufs{arena(kSlotBufs, 8ull * cmax * capg)},
