@@ -746,9 +746,13 @@ def cpu_batch_legs(args, data, graph, queries, gt, gpu_ids):
     cpu = {"value": sample / el, "unit": "queries/s", "cores": threads, "kind": "reference",
            **host_cpu(), "recall@10": recall_at_k(ids, gt[:sample]),
            "mean_distance_evals": float(np.mean(st["distance_evals"])),
-           "operating_point": f"per-query M={args.cpu_topm} p={args.cpu_width} {args.cpu_hash} "
-                              "hash (default: the reference's best recall>=0.95 grid point at "
-                              "1M x 96, profiles/r02_cpu_batch10k_sweep.txt)",
+           "operating_point": f"per-query M={args.cpu_topm} p={args.cpu_width} {args.cpu_hash} hash "
+                              + ("(the reference's best recall>=0.95 grid point at 1M x 96, "
+                                 "profiles/r02_cpu_batch10k_sweep.txt)"
+                                 if (args.cpu_topm, args.cpu_width) ==
+                                 (CPU_BATCH_POINT["topm"], CPU_BATCH_POINT["width"])
+                                 else "(--cpu-topm/--cpu-width: the reference's recall>=0.95 "
+                                      "point for this configuration)"),
            "sample": f"first {sample} of the {args.batch} batch queries, same index, "
                      f"fodg::batch_search per-query mode, {threads} threads"}
     return cpu, parity
